@@ -1,0 +1,72 @@
+"""Build the in-tree native libraries.
+
+  libfa3b.so           CUDA kernels + C ABI (include/fa3b.h), sm_100a only
+  libfa3b_flashlab.so  C++ host mirror of the reference's flashlab API
+                       (include/fa3b/flashlab_compat.hpp) over the C ABI
+
+Both are compiled with nvcc/g++ directly (no JIT cache), so the .so files
+travel with the repository snapshot to the GPU box.
+"""
+from __future__ import annotations
+
+import hashlib
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+CUDA_SOURCES = ["fa3b_capi.cu", "fwd_fp8.cu", "fp8_prepare.cu", "bwd.cu"]
+COMPAT_SOURCES = ["flashlab_compat.cpp"]
+
+
+def _digest(paths) -> str:
+    h = hashlib.sha256()
+    for p in sorted(paths):
+        h.update(p.name.encode())
+        h.update(p.read_bytes())
+    return h.hexdigest()
+
+
+def _inputs():
+    files = list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.cpp"))
+    files += list((ROOT / "include").rglob("*.h*"))
+    return files
+
+
+def _run(cmd):
+    print("[fa3b build]", " ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+
+
+def build(force: bool = False, verbose_ptxas: bool = False) -> Path:
+    out = PKG / "libfa3b.so"
+    compat = PKG / "libfa3b_flashlab.so"
+    stamp = PKG / ".build_stamp"
+    digest = _digest(_inputs())
+    if (not force and out.exists() and compat.exists() and stamp.exists()
+            and stamp.read_text() == digest):
+        return out
+    srcs = [str(CSRC / s) for s in CUDA_SOURCES if (CSRC / s).exists()]
+    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+           "-Xcompiler", "-fvisibility=hidden", "-shared", "-I", str(ROOT / "include"),
+           "-o", str(out), *srcs]
+    if verbose_ptxas:
+        cmd.insert(1, "-Xptxas=-v")
+    _run(cmd)
+    csrcs = [str(CSRC / s) for s in COMPAT_SOURCES if (CSRC / s).exists()]
+    if csrcs:
+        _run(["g++", "-O2", "-std=c++20", "-fPIC", "-shared", "-I", str(ROOT / "include"),
+              "-o", str(compat), *csrcs, f"-L{PKG}", "-lfa3b",
+              "-Wl,-rpath,$ORIGIN"])
+    stamp.write_text(digest)
+    return out
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose_ptxas="-v" in sys.argv)

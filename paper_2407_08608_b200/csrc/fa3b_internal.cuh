@@ -1,0 +1,24 @@
+// Host-side helpers shared by the C-ABI translation units.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "../../include/fa3b.h"
+
+namespace fa3b {
+
+extern thread_local int g_last_cuda_error;
+extern thread_local int g_last_launch_count;
+
+int cuda_fail(cudaError_t e);
+int make_tmap_4d(CUtensorMap* map, const fa3b_tensor4& t, int elem_bytes, int dim, int heads,
+                 int seqlen, int batch, int inner_elems, int rows);
+bool aligned16(const void* p);
+bool strides_ok(const fa3b_tensor4& t, int elem_bytes, int batch, int seqlen, int heads);
+int validate_problem(int batch, int heads_q, int heads_kv, int seqlen, int head_dim,
+                     double alpha);
+
+int launch_fwd_fp8(const fa3b_fwd_params& p, cudaStream_t stream);
+
+}  // namespace fa3b

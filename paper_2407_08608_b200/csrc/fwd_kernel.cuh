@@ -1,0 +1,348 @@
+// K1: attention forward for f16/bf16 on sm_100a.
+//
+// Replaces the reference's tiled forward (core/src/flash_fwd.cpp:18-232):
+// score_block (:57-71) is a tcgen05 SS-MMA into TMEM, online_softmax_step
+// (:18-48) runs in the softmax warpgroups, accumulate_output (:75-90) is a
+// tcgen05 TS-MMA with P read from TMEM, epilogue (:92-106) normalizes O and
+// writes the natural-log LSE, and active_col_blocks (:110-124) becomes the
+// per-tile KV block count.
+//
+// CTA layout (NT query tiles of 128 rows, KV blocks of 128 rows):
+//   warps [0, 4*NT)   softmax warpgroup t owns query tile t; thread r <-> row r
+//                     <-> TMEM lane r
+//   warp 4*NT         TMA producer: Q tiles once, then K_j, V_j through a ring
+//                     of STAGES shared-memory slots
+//   warp 4*NT+1       MMA issuer (one elected thread), TMEM allocator
+// TMEM (512 columns): S_t at [128 t, 128 t + 128), P_t (16-bit, 2 per column)
+// aliased onto the first 64 columns of S_t, O_t at [128 NT + D t, + D).
+//
+// Per tile the MMA order is  S(K_0) ; { PV(V_j) ; S(K_{j+1}) }_j , so the
+// arrival of S(K_{j+1}) implies PV(V_j) is complete (tcgen05.commit covers all
+// prior MMAs of the thread) and the softmax warpgroup may rescale O_t in place.
+// With NT = 2 the tensor core runs tile 1's GEMMs while tile 0 is in softmax
+// and vice versa (the paper's inter-warpgroup ping-pong).
+//
+// The running max is kept lazily: O and l are only rescaled when the block
+// max exceeds the max in use by more than 2^8 (log2 domain), so P <= 256.
+// The result equals the reference's rescale-every-block arithmetic up to
+// rounding (flash_fwd.cpp:36-45).
+#pragma once
+
+#include "sm100_ptx.cuh"
+
+namespace fa3b {
+
+struct FwdArgs {
+  int B, H, Hkv, N;
+  int group;          // H / Hkv
+  float scale_log2;   // |alpha| * log2(e)
+  void* o;
+  long long o_sb, o_ss, o_sh;  // element strides of O
+  int out_f32;
+  float* lse;         // [B, H, N] or nullptr
+};
+
+template <int D_, int NT_>
+struct FwdTraits {
+  static constexpr int D = D_;
+  static constexpr int NT = NT_;
+  static constexpr int BM = 128;
+  static constexpr int BN = 128;
+  static constexpr int CHUNK_BYTES = 128 * 128;  // 128 rows x 64 16-bit elements
+  static constexpr int CHUNKS = D / 64;
+  static constexpr int TILE_BYTES = CHUNKS * CHUNK_BYTES;
+  static constexpr int STAGES = D == 64 ? 8 : (D == 128 ? 4 : 2);
+  static constexpr int NUM_THREADS = NT * 128 + 64;
+  static constexpr int LOAD_WARP = NT * 4;
+  static constexpr int MMA_WARP = NT * 4 + 1;
+  static constexpr uint32_t TMEM_COLS = 512;
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_KV = NT * TILE_BYTES;
+  static constexpr int OFF_BAR = OFF_KV + STAGES * TILE_BYTES;
+  // q_full, kv_full[S], kv_empty[S], s_full[NT], p_full[NT], o_full[NT]
+  static constexpr int NUM_BARS = 1 + 2 * STAGES + 3 * NT;
+  static constexpr int SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16 + 1024;
+  static_assert(NT * (128 + D) <= 512, "TMEM budget");
+  static_assert(SMEM_BYTES <= 232448, "shared memory budget");
+  __host__ __device__ static constexpr int s_col(int t) { return t * 128; }
+  __host__ __device__ static constexpr int o_col(int t) { return NT * 128 + t * D; }
+};
+
+template <int D, int NT, bool CAUSAL, bool BF16>
+__global__ void __launch_bounds__(FwdTraits<D, NT>::NUM_THREADS, 1)
+    fa3b_fwd_kernel(const __grid_constant__ CUtensorMap tmQ,
+                    const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const FwdArgs args,
+                    const uint32_t idesc_qk, const uint32_t idesc_pv) {
+  using T = FwdTraits<D, NT>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + T::OFF_BAR);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;
+  uint64_t* kv_empty = kv_full + T::STAGES;
+  uint64_t* s_full = kv_empty + T::STAGES;
+  uint64_t* p_full = s_full + NT;
+  uint64_t* o_full = p_full + NT;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + T::NUM_BARS);
+
+  const int warp = static_cast<int>(ptx::warp_id());
+  const int nqb = gridDim.x;
+  const int qb = CAUSAL ? (nqb - 1 - static_cast<int>(blockIdx.x)) : static_cast<int>(blockIdx.x);
+  const int h = blockIdx.y;
+  const int b = blockIdx.z;
+  const int hkv = h / args.group;
+  const int N = args.N;
+  const int q_base = qb * NT * 128;
+  const int nkv = (N + 127) / 128;
+  int n_t[NT];
+  int n_max = 0;
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+    const int r0 = q_base + t * 128;
+    n_t[t] = (r0 < N) ? (CAUSAL ? min(nkv, r0 / 128 + 1) : nkv) : 0;
+    n_max = max(n_max, n_t[t]);
+  }
+
+  if (warp == T::MMA_WARP) {
+    if (ptx::lane_id() == 0) {
+      ptx::mbar_init(q_full, 1);
+      for (int s = 0; s < T::STAGES; ++s) {
+        ptx::mbar_init(&kv_full[s], 1);
+        ptx::mbar_init(&kv_empty[s], 1);
+      }
+      for (int t = 0; t < NT; ++t) {
+        ptx::mbar_init(&s_full[t], 1);
+        ptx::mbar_init(&p_full[t], 128);
+        ptx::mbar_init(&o_full[t], 1);
+      }
+      ptx::fence_mbar_init();
+    }
+    __syncwarp();
+    ptx::tmem_alloc<T::TMEM_COLS>(tmem_slot);
+  }
+  if (warp == T::LOAD_WARP && ptx::lane_id() == 0) {
+    ptx::prefetch_tmap(&tmQ);
+    ptx::prefetch_tmap(&tmK);
+    ptx::prefetch_tmap(&tmV);
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == T::LOAD_WARP) {
+    // ------------------------------------------------------------ producer
+    if (ptx::elect_one()) {
+      int nvalid = 0;
+#pragma unroll
+      for (int t = 0; t < NT; ++t) nvalid += n_t[t] > 0;
+      ptx::mbar_arrive_expect_tx(q_full, nvalid * T::TILE_BYTES);
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        if (n_t[t] == 0) continue;
+#pragma unroll
+        for (int c = 0; c < T::CHUNKS; ++c)
+          ptx::tma_load_4d(smem + T::OFF_Q + t * T::TILE_BYTES + c * T::CHUNK_BYTES, &tmQ,
+                           q_full, c * 64, h, q_base + t * 128, b, ptx::kEvictFirst);
+      }
+      int item = 0;
+      for (int j = 0; j < n_max; ++j) {
+#pragma unroll
+        for (int kv = 0; kv < 2; ++kv, ++item) {
+          const int slot = item % T::STAGES;
+          const uint32_t ph = (item / T::STAGES) & 1;
+          ptx::mbar_wait(&kv_empty[slot], ph ^ 1);
+          ptx::mbar_arrive_expect_tx(&kv_full[slot], T::TILE_BYTES);
+          uint8_t* dst = smem + T::OFF_KV + slot * T::TILE_BYTES;
+#pragma unroll
+          for (int c = 0; c < T::CHUNKS; ++c)
+            ptx::tma_load_4d(dst + c * T::CHUNK_BYTES, kv ? &tmV : &tmK, &kv_full[slot], c * 64,
+                             hkv, j * 128, b, ptx::kEvictLast);
+        }
+      }
+    }
+  } else if (warp == T::MMA_WARP) {
+    // ------------------------------------------------------------ MMA issuer
+    if (ptx::elect_one()) {
+      const uint32_t q_addr = ptx::smem_u32(smem + T::OFF_Q);
+      const uint32_t kv_addr = ptx::smem_u32(smem + T::OFF_KV);
+      auto issue_qk = [&](int t, int slot) {
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k >> 2) * T::CHUNK_BYTES + (k & 3) * 32;
+          const uint64_t a = ptx::sw128_desc(q_addr + t * T::TILE_BYTES + off, 16, 1024);
+          const uint64_t bd = ptx::sw128_desc(kv_addr + slot * T::TILE_BYTES + off, 16, 1024);
+          ptx::mma_f16_ss(tmem + T::s_col(t), a, bd, idesc_qk, k > 0 ? 1u : 0u);
+        }
+      };
+      auto issue_pv = [&](int t, int slot, bool acc) {
+#pragma unroll
+        for (int k = 0; k < 128 / 16; ++k) {
+          const uint64_t bd = ptx::sw128_desc(kv_addr + slot * T::TILE_BYTES + k * 16 * 128,
+                                              T::CHUNK_BYTES, 1024);
+          ptx::mma_f16_ts(tmem + T::o_col(t), tmem + T::s_col(t) + k * 8, bd, idesc_pv,
+                          (acc || k > 0) ? 1u : 0u);
+        }
+      };
+      ptx::mbar_wait(q_full, 0);
+      if (n_max > 0) {
+        ptx::mbar_wait(&kv_full[0], 0);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          if (n_t[t] == 0) continue;
+          issue_qk(t, 0);
+          ptx::mma_commit(&s_full[t]);
+        }
+        ptx::mma_commit(&kv_empty[0]);
+      }
+      for (int j = 0; j < n_max; ++j) {
+        const int item_v = 2 * j + 1, item_k = 2 * j + 2;
+        const int slot_v = item_v % T::STAGES, slot_k = item_k % T::STAGES;
+        ptx::mbar_wait(&kv_full[slot_v], (item_v / T::STAGES) & 1);
+        bool k_ready = false;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          if (j >= n_t[t]) continue;
+          ptx::mbar_wait(&p_full[t], j & 1);
+          ptx::tc_fence_after();
+          issue_pv(t, slot_v, j > 0);
+          if (j + 1 < n_t[t]) {
+            if (!k_ready) {
+              ptx::mbar_wait(&kv_full[slot_k], (item_k / T::STAGES) & 1);
+              ptx::tc_fence_after();
+              k_ready = true;
+            }
+            issue_qk(t, slot_k);
+            ptx::mma_commit(&s_full[t]);
+          } else {
+            ptx::mma_commit(&o_full[t]);
+          }
+        }
+        ptx::mma_commit(&kv_empty[slot_v]);
+        if (k_ready) ptx::mma_commit(&kv_empty[slot_k]);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax
+    const int t = warp >> 2;
+    const int r = threadIdx.x & 127;
+    const uint32_t lane_base = static_cast<uint32_t>(32 * (warp & 3)) << 16;
+    const uint32_t tS = tmem + lane_base + T::s_col(t);
+    const uint32_t tO = tmem + lane_base + T::o_col(t);
+    const int q_row = q_base + t * 128 + r;
+    const int nt = n_t[t];
+    const float sl2 = args.scale_log2;
+    float m_use = -INFINITY;  // running max in use, scaled log2 units
+    float l = 0.f;
+    for (int j = 0; j < nt; ++j) {
+      ptx::mbar_wait(&s_full[t], j & 1);
+      ptx::tc_fence_after();
+      uint32_t sr[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        ptx::tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
+      ptx::tmem_wait_ld();
+      float s[128];
+#pragma unroll
+      for (int i = 0; i < 128; ++i) s[i] = __uint_as_float(sr[i]);
+      const int kv0 = j * 128;
+      const bool need_mask = (kv0 + 128 > N) || (CAUSAL && j == nt - 1);
+      if (need_mask) {
+        const int lim = (CAUSAL ? min(q_row + 1, N) : N) - kv0;
+#pragma unroll
+        for (int i = 0; i < 128; ++i) s[i] = (i < lim) ? s[i] : -INFINITY;
+      }
+      float mx = s[0];
+#pragma unroll
+      for (int i = 1; i < 128; ++i) mx = fmaxf(mx, s[i]);
+      const float m_new = fmaxf(m_use, mx * sl2);
+      const bool resc = m_new > m_use + 8.f;
+      const float m_cur = resc ? m_new : m_use;
+      const float factor = resc ? ptx::ex2(m_use - m_new) : 1.f;
+      const float msub = (m_cur == -INFINITY) ? 0.f : m_cur;
+      float sum0 = 0.f, sum1 = 0.f;
+      uint32_t pk[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        const float p0 = ptx::ex2(fmaf(s[2 * i], sl2, -msub));
+        const float p1 = ptx::ex2(fmaf(s[2 * i + 1], sl2, -msub));
+        sum0 += p0;
+        sum1 += p1;
+        pk[i] = BF16 ? ptx::pack_bf16(p0, p1) : ptx::pack_f16(p0, p1);
+      }
+      l = l * factor + (sum0 + sum1);
+      ptx::tmem_st32(tS, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+      ptx::tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
+      if (j > 0 && __any_sync(0xffffffffu, resc)) {
+        // PV(V_{j-1}) is complete (see header); rescale this row of O_t.
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t ov[32];
+          ptx::tmem_ld32(tO + c * 32, ov);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * factor);
+          ptx::tmem_st32(tO + c * 32, ov);
+        }
+      }
+      ptx::tmem_wait_st();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&p_full[t]);
+      m_use = m_cur;
+    }
+    if (nt > 0) {
+      // ---------------------------------------------------------- epilogue
+      ptx::mbar_wait(&o_full[t], 0);
+      ptx::tc_fence_after();
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      const bool row_ok = q_row < N;
+      const size_t obase = static_cast<size_t>(b) * args.o_sb +
+                           static_cast<size_t>(q_row) * args.o_ss +
+                           static_cast<size_t>(h) * args.o_sh;
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t ov[32];
+        ptx::tmem_ld32(tO + c * 32, ov);
+        ptx::tmem_wait_ld();
+        if (!row_ok) continue;
+        if (args.out_f32) {
+          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(args.o) + obase + c * 32);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            dst[i] = make_float4(__uint_as_float(ov[4 * i]) * inv,
+                                 __uint_as_float(ov[4 * i + 1]) * inv,
+                                 __uint_as_float(ov[4 * i + 2]) * inv,
+                                 __uint_as_float(ov[4 * i + 3]) * inv);
+        } else {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float a = __uint_as_float(ov[2 * i]) * inv;
+            const float bb = __uint_as_float(ov[2 * i + 1]) * inv;
+            pk[i] = BF16 ? ptx::pack_bf16(a, bb) : ptx::pack_f16(a, bb);
+          }
+          uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(args.o) + obase + c * 32);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+        }
+      }
+      if (row_ok && args.lse != nullptr) {
+        const float lse = l > 0.f ? (m_use + log2f(l)) * 0.69314718055994531f : -INFINITY;
+        args.lse[(static_cast<size_t>(b) * args.H + h) * N + q_row] = lse;
+      }
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == T::MMA_WARP) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<T::TMEM_COLS>(tmem);
+  }
+}
+
+}  // namespace fa3b
