@@ -1,0 +1,416 @@
+"""Benchmark of the fa3b hot path (BASELINE.json metric: attention fwd/bwd
+TFLOPs/s vs seqlen at hdim 128, % of B200 tensor peak).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Step = one forward pass of the C2 workload shard (BF16, hdim 128, seqlen
+8192, batch 2 x 16 heads = 16k tokens, hidden 2048, non-causal) through the
+C ABI (fa3b_fwd). Multi-GPU (torchrun) is weak scaling: every rank runs its
+own batch shard, no data-path collective (attention shards by batch x head);
+the only cross-rank traffic is the barrier and the max-over-ranks of the
+device time.
+
+--impl reference times the reference's own CPU implementation
+(oracle/_ref/libflashlab_ref.so = flashlab flash_fwd_2stage compiled from
+its sources; the C restatement if that library is absent) on the same
+workload, one (batch, head) unit per host process.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "attention fwd/bwd TFLOPs/s (BF16, FP8) vs seqlen at hdim 128; % of B200 tensor peak"
+WORKLOAD = dict(name="C2 bf16 fwd hdim128 seqlen8192", batch=2, heads=16, heads_kv=16,
+                seqlen=8192, head_dim=128, causal=False)
+
+
+def flops_fwd(B, H, N, D, causal):
+    f = 4 * N * N * D * H * B  # flash_fwd.hpp:69-73
+    return f // 2 if causal else f
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get("bf16_tflops", 1590.0), d.get("hbm_gbs", 6650.0), "measured"
+    return 1590.0, 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    def __init__(self, index: int):
+        self.samples = []
+        self.reasons = set()
+        self._stop = threading.Event()
+        self._t = None
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join()
+
+    def summary(self):
+        s = sorted(self.samples)
+        return {"sm_mhz": s[len(s) // 2] if s else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(s)}
+
+
+# ------------------------------------------------------------ reference arm
+_REF = None
+
+
+def _ref_worker_init(n, d, use_ref):
+    global _REF
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as O
+    impl = O.Ref() if use_ref else O.Port()
+    q = impl.sample_gaussian(n, d, impl.substream(1, 1))
+    k = impl.sample_gaussian(n, d, impl.substream(1, 2))
+    v = impl.sample_gaussian(n, d, impl.substream(1, 3))
+    _REF = (impl, use_ref, q, k, v)
+
+
+def _ref_worker_run(causal):
+    impl, use_ref, q, k, v = _REF
+    t0 = time.perf_counter()
+    if use_ref:
+        impl.flash_fwd(q, k, v, causal=causal, tile=(64, 64), schedule=1)  # flash_fwd_2stage
+    else:
+        impl.flash_fwd(q, k, v, causal=causal, tile=(64, 64))
+    return time.perf_counter() - t0
+
+
+class CpuReference:
+    """The reference CPU path: one (batch, head) unit per process, P processes
+    (threads in one process scale poorly)."""
+
+    def __init__(self, n, d, causal, procs=None):
+        import multiprocessing as mp
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import oracle as O
+        self.use_ref = O.Ref.available()
+        self.kind = "reference" if self.use_ref else "port"
+        self.n, self.d, self.causal = n, d, causal
+        self.procs = procs or len(os.sched_getaffinity(0)) or 1
+        ctx = mp.get_context("spawn")
+        self.pool = ctx.Pool(self.procs, initializer=_ref_worker_init,
+                             initargs=(n, d, self.use_ref))
+
+    def step(self):
+        t0 = time.perf_counter()
+        self.pool.map(_ref_worker_run, [self.causal] * self.procs, chunksize=1)
+        return time.perf_counter() - t0
+
+    def flops_per_step(self):
+        return flops_fwd(1, 1, self.n, self.d, self.causal) * self.procs
+
+    def sample_desc(self):
+        lib = "oracle/_ref flashlab flash_fwd_2stage" if self.use_ref else "oracle port"
+        return (f"{self.procs} processes x 1 (batch, head) unit each: N={self.n}, d={self.d}, "
+                f"causal={int(self.causal)}, FP64, tile 64x64 ({lib})")
+
+    def close(self):
+        self.pool.terminate()
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    w = WORKLOAD
+    # Bound the whole run to a few minutes: a unit at N=8192 costs ~6 s of one
+    # core; shorter sequence samples keep the same per-core FLOP rate.
+    total = args.steps + args.warmup
+    n_s = w["seqlen"] if total <= 20 else (4096 if total <= 80 else 2048)
+    ref = CpuReference(n_s, w["head_dim"], w["causal"])
+    try:
+        for _ in range(args.warmup):
+            ref.step()
+        times = [ref.step() for _ in range(args.steps)]
+    finally:
+        ref.close()
+    sec = sum(times) / len(times)
+    value = ref.flops_per_step() / sec / 1e12
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w["name"], "global_batch": w["batch"] * world,
+                   "seq_len": w["seqlen"], "heads": w["heads"], "head_dim": w["head_dim"],
+                   "causal": w["causal"], "parallelism": "host processes",
+                   "cpu": cpu_model()},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": ref.procs,
+                         "kind": ref.kind, "sample": ref.sample_desc()},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------- our arm
+def time_fwd(api, torch, q, k, v, causal, iters, warmup, stream):
+    for _ in range(warmup):
+        api.fwd(q, k, v, causal=causal, stream=stream)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(iters)]
+    for a, b in ev:
+        a.record(stream)
+        api.fwd(q, k, v, causal=causal, stream=stream)
+        b.record(stream)
+    torch.cuda.synchronize()
+    return sum(a.elapsed_time(b) for a, b in ev) / iters
+
+
+def sweep(api, torch, dev, stream):
+    """C2 sweep (16k tokens per point, hidden 2048) plus C5 (Llama-3-70B GQA)."""
+    out = []
+    pts = [(n, 128, c) for n in (512, 1024, 2048, 4096, 8192, 16384) for c in (False, True)]
+    pts += [(8192, 64, False), (8192, 64, True), (8192, 256, False), (8192, 256, True)]
+    for n, d, causal in pts:
+        B, H = 16384 // n, 2048 // d
+        q, k, v = (torch.randn(B, n, H, d, device=dev, dtype=torch.bfloat16) for _ in range(3))
+        ms = time_fwd(api, torch, q, k, v, causal, 10, 3, stream)
+        out.append({"pass": "fwd", "dtype": "bf16", "seqlen": n, "head_dim": d, "batch": B,
+                    "heads": H, "causal": causal,
+                    "tflops": flops_fwd(B, H, n, d, causal) / ms / 1e9, "ms": ms})
+        del q, k, v
+    q = torch.randn(1, 8192, 64, 128, device=dev, dtype=torch.bfloat16)
+    k, v = (torch.randn(1, 8192, 8, 128, device=dev, dtype=torch.bfloat16) for _ in range(2))
+    for causal in (False, True):
+        ms = time_fwd(api, torch, q, k, v, causal, 10, 3, stream)
+        out.append({"pass": "fwd", "dtype": "bf16", "workload": "C5 llama3-70b gqa 64/8",
+                    "seqlen": 8192, "head_dim": 128, "batch": 1, "heads": 64, "heads_kv": 8,
+                    "causal": causal, "tflops": flops_fwd(1, 64, 8192, 128, causal) / ms / 1e9,
+                    "ms": ms})
+    return out
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2407_08608_b200 import _lib, api
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    lib = _lib.load()
+    w = WORKLOAD
+    B, H, Hkv, N, D, causal = (w["batch"], w["heads"], w["heads_kv"], w["seqlen"],
+                               w["head_dim"], w["causal"])
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    q = torch.randn(B, N, H, D, device=dev, dtype=torch.bfloat16, generator=gen)
+    k = torch.randn(B, N, Hkv, D, device=dev, dtype=torch.bfloat16, generator=gen)
+    v = torch.randn(B, N, Hkv, D, device=dev, dtype=torch.bfloat16, generator=gen)
+    o = torch.empty_like(q)
+    lse = torch.empty(B, H, N, device=dev, dtype=torch.float32)
+    stream = torch.cuda.Stream(device=dev)
+    step_flops = flops_fwd(B, H, N, D, causal)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            api.fwd(q, k, v, causal=causal, out=o, lse=lse, stream=stream)
+    torch.cuda.synchronize()
+
+    # ---------------- timed region: exactly K steps, device time, max over ranks
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    t_all0, t_all1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    sampler = ClockSampler(local_rank)
+    barrier()
+    torch.cuda.synchronize()
+    with sampler:
+        t_all0.record(stream)
+        for a, b in ev:
+            a.record(stream)
+            api.fwd(q, k, v, causal=causal, out=o, lse=lse, stream=stream)
+            launches += lib.fa3b_last_launch_count()
+            b.record(stream)
+        t_all1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    total_ms = t_all0.elapsed_time(t_all1)
+    kernel_ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    t = torch.tensor([total_ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = step_flops * world / (ms_per_step * 1e-3) / 1e12
+
+    # ---------------- end to end through the public API with host buffers
+    qh, kh, vh = (x.cpu().pin_memory() for x in (q, k, v))
+    oh = torch.empty(o.shape, dtype=o.dtype).pin_memory()
+    lh = torch.empty(lse.shape, dtype=lse.dtype).pin_memory()
+    e2e_steps = max(3, min(args.steps, 10))
+
+    def e2e_step():
+        qd = qh.to(dev, non_blocking=True)
+        kd = kh.to(dev, non_blocking=True)
+        vd = vh.to(dev, non_blocking=True)
+        od, ld = api.fwd(qd, kd, vd, causal=causal, stream=stream)
+        oh.copy_(od, non_blocking=True)
+        lh.copy_(ld, non_blocking=True)
+
+    with torch.cuda.stream(stream):
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    t = torch.tensor([e2e_ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+    h2d = sum(x.numel() * x.element_size() for x in (qh, kh, vh))
+    d2h = oh.numel() * oh.element_size() + lh.numel() * lh.element_size()
+
+    if rank != 0:
+        return 0
+    peak, hbm, peak_src = measured_peaks()
+    achieved = step_flops / (kernel_ms * 1e-3) / 1e12
+    traffic = None
+    prof = ROOT / "profiles" / "ncu_summary.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("fwd_c2_d128", {}).get("dram_bytes")
+        except (ValueError, OSError):
+            traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (torch.randn bf16 Q/K/V on device)",
+        "config": {"workload": w["name"], "global_batch": B * world, "seq_len": N, "heads": H,
+                   "heads_kv": Hkv, "head_dim": D, "causal": causal,
+                   "parallelism": f"batch-sharded x{world} (no collectives)",
+                   "l2": "no flush; inputs larger than L2 (Q+K+V+O = "
+                         f"{4 * q.numel() * 2 >> 20} MiB > 126 MB)"},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json)",
+                     "kernel": "fa3b_fwd_kernel<128,2,false,bf16>",
+                     "algorithmic_flops_per_launch": step_flops,
+                     "kernel_ms": kernel_ms},
+        "e2e": {"value": step_flops * world / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                "path": "pinned host bf16 -> H2D -> fa3b_fwd (C ABI) -> D2H O + LSE"},
+        "gpu_launches": launches,
+        "clocks": sampler.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        ref = CpuReference(N, D, causal, procs=args.cpu_procs)
+        try:
+            secs = ref.step()  # inputs are generated in the pool initializer
+        finally:
+            ref.close()
+        line["cpu_baseline"] = {"value": ref.flops_per_step() / secs / 1e12, "unit": "TFLOP/s",
+                                "cores": ref.procs, "kind": ref.kind,
+                                "sample": ref.sample_desc() + f"; {cpu_model()}"}
+    if world == 1 and not args.no_sweep:
+        with torch.cuda.stream(stream):
+            line["sweep"] = sweep(api, torch, dev, stream)
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-procs", type=int, default=None)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        return run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -34,6 +34,7 @@ void orc_sign_vector(size_t n, uint64_t seed, double* out);
 
 /* formats.cpp:45-61 */
 double orc_round_to(double x, int fmt, int overflow_infinite);
+void orc_round_array(const double* in, size_t n, int fmt, double* out);
 
 /* hadamard.cpp:11-64, fp8_attention.cpp:33-42 */
 int orc_fwht(double* v, size_t n);

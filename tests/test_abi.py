@@ -1,0 +1,125 @@
+"""The C-ABI surface, checked without a GPU: the library loads, exports every
+symbol include/fa3b.h declares, the ctypes structs match the C layout, and
+argument validation returns the reference's error cases before any device
+work happens."""
+from __future__ import annotations
+
+import ctypes
+import math
+import re
+import subprocess
+from pathlib import Path
+
+import pytest
+
+from paper_2407_08608_b200 import _lib
+
+ROOT = Path(__file__).resolve().parents[1]
+HEADER = ROOT / "include" / "fa3b.h"
+
+
+def test_header_declares_exactly_the_bound_symbols():
+    text = HEADER.read_text()
+    declared = set(re.findall(r"FA3B_API\s+[\w\s\*]+?\b(fa3b_\w+)\s*\(", text))
+    assert declared == set(_lib.EXPORTED_SYMBOLS)
+
+
+def test_library_exports_every_symbol(fa3b_lib):
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_lib.LIB_PATH)], check=True,
+                         capture_output=True, text=True).stdout
+    exported = {line.split()[-1] for line in out.splitlines() if " T " in line}
+    missing = set(_lib.EXPORTED_SYMBOLS) - exported
+    assert not missing, missing
+    # nothing but the C ABI leaks out (kernels and helpers stay hidden)
+    assert {s for s in exported if s.startswith("fa3b_")} == set(_lib.EXPORTED_SYMBOLS)
+
+
+def test_library_carries_sm100a_tcgen05_code(fa3b_lib):
+    sass = subprocess.run(["cuobjdump", "-sass", str(_lib.LIB_PATH)], check=True,
+                          capture_output=True, text=True).stdout
+    assert "sm_100a" in subprocess.run(["cuobjdump", "-lelf", str(_lib.LIB_PATH)], check=True,
+                                       capture_output=True, text=True).stdout
+    for mnemonic in ("UTCHMMA", "UTMALDG", "LDTM", "STTM"):
+        assert mnemonic in sass, mnemonic
+    assert "HMMA" not in sass.replace("UTCHMMA", ""), "legacy mma.sync path present"
+
+
+def test_struct_layout_matches_c(tmp_path):
+    src = tmp_path / "sizes.c"
+    src.write_text(
+        '#include <stdio.h>\n#include <stddef.h>\n#include "fa3b.h"\n'
+        "int main(void){printf(\"%zu %zu %zu %zu %zu %zu %zu %zu\\n\","
+        " sizeof(fa3b_fwd_params), sizeof(fa3b_fp8_prepare_params), sizeof(fa3b_bwd_params),"
+        " sizeof(fa3b_bwd_preprocess_params), sizeof(fa3b_tensor4),"
+        " offsetof(fa3b_fwd_params, stream), offsetof(fa3b_bwd_params, stream),"
+        " offsetof(fa3b_fp8_prepare_params, stream));return 0;}\n")
+    exe = tmp_path / "sizes"
+    subprocess.run(["gcc", "-I", str(ROOT / "include"), "-o", str(exe), str(src)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], check=True, capture_output=True,
+                                          text=True).stdout.split()]
+    want = [ctypes.sizeof(_lib.FwdParams), ctypes.sizeof(_lib.Fp8PrepareParams),
+            ctypes.sizeof(_lib.BwdParams), ctypes.sizeof(_lib.BwdPreprocessParams),
+            ctypes.sizeof(_lib.Tensor4), _lib.FwdParams.stream.offset,
+            _lib.BwdParams.stream.offset, _lib.Fp8PrepareParams.stream.offset]
+    assert got == want
+
+
+def test_flop_counts_and_version(fa3b_lib):
+    """flash_fwd.hpp:69-77 / test_flash_fwd.cpp:224-230."""
+    assert fa3b_lib.fa3b_flops_forward(512, 64, 32, 0) == 2147483648
+    assert fa3b_lib.fa3b_flops_forward(512, 64, 32, 1) == 1073741824
+    assert fa3b_lib.fa3b_flops_backward(512, 64, 32, 0) == 2147483648 * 5 // 2
+    assert fa3b_lib.fa3b_flops_forward(1, 1, 1, 0) == 4
+    assert fa3b_lib.fa3b_abi_version() == 1
+
+
+def _fwd_params(**kw):
+    p = _lib.FwdParams()
+    p.struct_size = ctypes.sizeof(_lib.FwdParams)
+    p.batch, p.heads_q, p.heads_kv, p.seqlen, p.head_dim = 1, 2, 2, 128, 64
+    p.in_dtype = p.out_dtype = _lib.BF16
+    for name in ("q", "k", "v", "o"):
+        setattr(p, name, _lib.Tensor4(4096, 2 * 64 * 128, 2 * 64, 64))
+    p.alpha = 0.125
+    for key, val in kw.items():
+        setattr(p, key, val)
+    return p
+
+
+@pytest.mark.parametrize("overrides,status,message", [
+    ({"alpha": 0.0}, -4, "attention: alpha must be finite and nonzero"),
+    ({"alpha": math.nan}, -4, "attention: alpha must be finite and nonzero"),
+    ({"alpha": math.inf}, -4, "attention: alpha must be finite and nonzero"),
+    ({"seqlen": 0}, -1, "attention: empty inputs"),
+    ({"head_dim": 96}, -5, "head dimension must be 64, 128 or 256"),
+    ({"heads_kv": 3}, -6, "gqa_head_map: heads must be a multiple of kv_heads"),
+    ({"struct_size": 8}, -15, "struct size"),
+    ({"in_dtype": 3}, -8, "dtype"),
+    ({"q": _lib.Tensor4(4098, 2 * 64 * 128, 2 * 64, 64)}, -7, "16-byte aligned"),
+    ({"k": _lib.Tensor4(0, 0, 0, 0)}, -9, "NULL"),
+])
+def test_fwd_validation_errors(fa3b_lib, overrides, status, message):
+    p = _fwd_params(**overrides)
+    rc = fa3b_lib.fa3b_fwd(ctypes.byref(p))
+    assert rc == status
+    assert message in fa3b_lib.fa3b_error_string(rc).decode()
+    assert fa3b_lib.fa3b_last_launch_count() == 0
+
+
+def test_error_strings_cover_reference_messages(fa3b_lib):
+    # wording of the reference's std::invalid_argument cases
+    want = {-1: "attention: empty inputs", -2: "attention: head dimension mismatch",
+            -3: "attention: sequence length mismatch",
+            -4: "attention: alpha must be finite and nonzero",
+            -10: "flash_bwd: dO shape mismatch", -11: "flash_bwd: forward output shape mismatch",
+            -12: "random_dh_transform: dim must be a power of two",
+            -13: "TileConfig: block sizes must be positive"}
+    for code, msg in want.items():
+        assert fa3b_lib.fa3b_error_string(code).decode() == msg
+
+
+def test_load_fails_loudly_without_library(tmp_path, monkeypatch):
+    monkeypatch.setattr(_lib, "_lib", None)
+    monkeypatch.setenv("FA3B_LIB", str(tmp_path / "missing.so"))
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        _lib.load()

@@ -1,0 +1,188 @@
+"""K1 forward on the device against the CPU oracle.
+
+Tolerance (stated per SURVEY.md §8(c)): with both sides fed the same
+bf16/fp16-rounded inputs,
+    RMSE(gpu - fp64)   <= 2 * RMSE(emu - fp64) + 1e-6
+    max|gpu - fp64|    <= 8 * max|emu - fp64| + 1e-6
+    max|LSE_gpu - LSE| <= 1e-3
+where fp64 is the reference's exact attention (reference_attention_o) and
+emu is the oracle's tiled low-precision forward (lowprec.cpp:166-240 in the
+input format: fp32 scores/softmax/accumulator, P rounded to the format,
+output rounded to the format).
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+from _util import FMT, make_inputs, maxabs, rmse, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+def _api():
+    from paper_2407_08608_b200 import api
+    return api
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dtype(fmt):
+    torch = _torch()
+    return torch.bfloat16 if fmt == "bf16" else torch.float16
+
+
+def _oracle_fwd(port, q, k, v, alpha, causal, fmt):
+    B, N, H, D = q.shape
+    Hkv = k.shape[2]
+    g = H // Hkv
+    ref_o = np.empty_like(q)
+    ref_l = np.empty((B, H, N))
+    emu_o = np.empty_like(q)
+    for b in range(B):
+        for h in range(H):
+            args = (q[b, :, h], k[b, :, h // g], v[b, :, h // g])
+            ref_o[b, :, h], ref_l[b, h] = port.reference_attention(*args, alpha=alpha,
+                                                                   causal=causal)
+            emu_o[b, :, h], _ = port.lowprec_flash_fwd(*args, alpha=alpha, causal=causal,
+                                                       tile=(128, 128), fmt=FMT[fmt])
+    return ref_o, ref_l, emu_o
+
+
+CASES = [
+    # B, H, Hkv, N, D, causal, fmt, schedule, alpha
+    pytest.param(2, 8, 8, 512, 64, False, "fp16", "pingpong", None, id="C1-B2H8N512d64-fp16"),
+    pytest.param(1, 2, 2, 1000, 128, True, "bf16", "pingpong", None, id="ragged-causal-d128"),
+    pytest.param(1, 2, 1, 777, 256, True, "bf16", "basic", None, id="d256-gqa-causal"),
+    pytest.param(1, 4, 2, 384, 128, False, "bf16", "basic", -0.09, id="negative-alpha"),
+    pytest.param(2, 2, 2, 130, 64, True, "fp16", "pingpong", 0.3, id="tile1-partial"),
+    pytest.param(1, 2, 2, 100, 64, False, "bf16", "pingpong", None, id="N-lt-128"),
+    pytest.param(1, 1, 1, 1, 64, False, "bf16", "pingpong", None, id="N1"),
+    pytest.param(1, 2, 2, 640, 128, True, "fp16", "3stage", None, id="3stage-alias"),
+    pytest.param(1, 2, 2, 512, 256, False, "fp16", "basic", 0.02, id="d256-fp16"),
+]
+
+
+@pytest.mark.parametrize("B,H,Hkv,N,D,causal,fmt,sched,alpha", CASES)
+def test_fwd_matches_oracle(port, cuda, B, H, Hkv, N, D, causal, fmt, sched, alpha):
+    api = _api()
+    alpha = 1.0 / math.sqrt(D) if alpha is None else alpha
+    q, k, v = make_inputs(port, B, H, Hkv, N, D, seed=1000 + N + D, fmt=fmt)
+    dt = _dtype(fmt)
+    o, lse = api.fwd(to_dev(q, dt), to_dev(k, dt), to_dev(v, dt), causal=causal, alpha=alpha,
+                     schedule=sched)
+    o = o.float().cpu().numpy()
+    lse = lse.cpu().numpy()
+    ref_o, ref_l, emu_o = _oracle_fwd(port, q, k, v, alpha, causal, fmt)
+    e_gpu, e_emu = rmse(o, ref_o), rmse(emu_o, ref_o)
+    m_gpu, m_emu = maxabs(o, ref_o), maxabs(emu_o, ref_o)
+    assert e_gpu <= 2 * e_emu + 1e-6, (e_gpu, e_emu)
+    assert m_gpu <= 8 * m_emu + 1e-6, (m_gpu, m_emu)
+    assert maxabs(lse, ref_l) <= 1e-3
+
+
+def test_fwd_fp32_output_is_tighter(port, cuda):
+    api = _api()
+    torch = _torch()
+    q, k, v = make_inputs(port, 1, 2, 2, 300, 128, seed=77)
+    o, lse = api.fwd(to_dev(q, torch.bfloat16), to_dev(k, torch.bfloat16),
+                     to_dev(v, torch.bfloat16), causal=True, out_dtype=torch.float32)
+    ref_o, ref_l, emu_o = _oracle_fwd(port, q, k, v, 1 / math.sqrt(128), True, "bf16")
+    # no output rounding: only P's bf16 rounding and fp32 accumulation remain
+    assert rmse(o.cpu().numpy(), ref_o) <= 0.5 * rmse(emu_o, ref_o)
+    assert maxabs(lse.cpu().numpy(), ref_l) <= 1e-4
+
+
+@pytest.mark.parametrize("name", ["dev_n200_d64_causal", "dev_n160_d128"])
+def test_fwd_against_reference_golden(golden, cuda, name):
+    """Straight against outputs of the reference library (tests/golden)."""
+    api = _api()
+    torch = _torch()
+    n, d, causal, a = golden[f"{name}_meta"]
+    q, k, v = (golden[f"{name}_{x}"][None, :, None, :] for x in ("q", "k", "v"))
+    o, lse = api.fwd(to_dev(q, torch.bfloat16), to_dev(k, torch.bfloat16),
+                     to_dev(v, torch.bfloat16), causal=bool(causal), alpha=float(a),
+                     out_dtype=torch.float32)
+    assert maxabs(o.cpu().numpy()[0, :, 0], golden[f"{name}_o"]) < 2e-2
+    assert rmse(o.cpu().numpy()[0, :, 0], golden[f"{name}_o"]) < 2e-3
+    assert maxabs(lse.cpu().numpy()[0, 0], golden[f"{name}_lse"]) < 1e-4
+
+
+def test_gqa_mapping_equals_duplication_bitwise(port, cuda):
+    """acceptance criterion 10 (acceptance_main.cpp:357-383): bit-exact."""
+    api = _api()
+    torch = _torch()
+    for hkv in (4, 2, 1):
+        q, k, v = make_inputs(port, 1, 4, hkv, 256, 64, seed=500 + hkv)
+        qd, kd, vd = (to_dev(x, torch.bfloat16) for x in (q, k, v))
+        o1, l1 = api.fwd(qd, kd, vd)
+        g = 4 // hkv
+        o2, l2 = api.fwd(qd, kd.repeat_interleave(g, 2).contiguous(),
+                         vd.repeat_interleave(g, 2).contiguous())
+        assert torch.equal(o1, o2) and torch.equal(l1, l2)
+
+
+def test_schedules_and_reruns_bit_identical(port, cuda):
+    """The reference demands bit-identical schedules (test_flash_fwd.cpp:152-196)
+    and deterministic reruns; the device kernels keep both."""
+    api = _api()
+    torch = _torch()
+    for causal in (False, True):
+        q, k, v = (to_dev(x, torch.bfloat16) for x in make_inputs(port, 1, 2, 2, 700, 128, 9))
+        a = api.fwd(q, k, v, causal=causal, schedule="pingpong")
+        b = api.fwd(q, k, v, causal=causal, schedule="basic")
+        c = api.fwd(q, k, v, causal=causal, schedule="pingpong")
+        assert torch.equal(a[0], c[0]) and torch.equal(a[1], c[1])
+        assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+def test_strided_inputs(port, cuda):
+    """Q/K/V as views into a packed [B, N, 3, H, D] buffer."""
+    api = _api()
+    torch = _torch()
+    q, k, v = make_inputs(port, 2, 4, 4, 300, 64, seed=3)
+    qkv = torch.stack([to_dev(x, torch.bfloat16) for x in (q, k, v)], dim=2)
+    o1, l1 = api.fwd(qkv[:, :, 0], qkv[:, :, 1], qkv[:, :, 2], causal=True)
+    o2, l2 = api.fwd(*(qkv[:, :, i].contiguous() for i in range(3)), causal=True)
+    assert torch.equal(o1, o2) and torch.equal(l1, l2)
+
+
+@pytest.mark.parametrize("D,causal", [(128, False), (128, True), (64, True), (256, False)])
+def test_full_size_against_torch_rows(cuda, D, causal):
+    """C2 at N = 16k (B = 1, H = 2048 / D): a sample of query rows checked
+    against fp32 torch attention over all 16k keys."""
+    api = _api()
+    torch = _torch()
+    N, H = 16384, 2048 // D
+    gen = torch.Generator(device="cuda").manual_seed(D + causal)
+    q, k, v = (torch.randn(1, N, H, D, device="cuda", generator=gen, dtype=torch.bfloat16)
+               for _ in range(3))
+    o, lse = api.fwd(q, k, v, causal=causal)
+    rows = torch.cat([torch.arange(0, 64), torch.randint(64, N, (192,), generator=gen,
+                                                          device="cuda").cpu()]).cuda()
+    alpha = 1 / math.sqrt(D)
+    for h in range(0, H, max(1, H // 4)):
+        s = alpha * q[0, rows, h].float() @ k[0, :, h].float().T
+        if causal:
+            s = s.masked_fill(torch.arange(N, device="cuda")[None, :] > rows[:, None], -math.inf)
+        ref_l = torch.logsumexp(s, -1)
+        ref_o = torch.softmax(s, -1) @ v[0, :, h].float()
+        assert (o[0, rows, h].float() - ref_o).abs().max().item() < 2e-2
+        assert (lse[0, h, rows] - ref_l).abs().max().item() < 1e-3
+
+
+def test_fwd_rejects_bad_arguments(cuda):
+    api = _api()
+    torch = _torch()
+    from paper_2407_08608_b200._lib import Fa3bError
+    q = torch.zeros(1, 128, 2, 96, device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(Fa3bError, match="head dimension"):
+        api.fwd(q, q, q)
+    q = torch.zeros(1, 128, 2, 64, device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(Fa3bError, match="alpha"):
+        api.fwd(q, q, q, alpha=0.0)
