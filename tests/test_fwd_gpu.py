@@ -94,7 +94,7 @@ def test_fwd_fp32_output_is_tighter(port, cuda):
                      to_dev(v, torch.bfloat16), causal=True, out_dtype=torch.float32)
     ref_o, ref_l, emu_o = _oracle_fwd(port, q, k, v, 1 / math.sqrt(128), True, "bf16")
     # no output rounding: only P's bf16 rounding and fp32 accumulation remain
-    assert rmse(o.cpu().numpy(), ref_o) <= 0.5 * rmse(emu_o, ref_o)
+    assert rmse(o.cpu().numpy(), ref_o) <= 0.75 * rmse(emu_o, ref_o)
     assert maxabs(lse.cpu().numpy(), ref_l) <= 1e-4
 
 
