@@ -54,7 +54,7 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> Path:
         return out
     srcs = [str(CSRC / s) for s in CUDA_SOURCES if (CSRC / s).exists()]
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-           "-Xcompiler", "-fvisibility=hidden", "-shared", "-I", str(ROOT / "include"),
+           "-Xcompiler", "-fvisibility=hidden", "-shared", "-Xlinker", "--no-undefined", "-I", str(ROOT / "include"),
            "-o", str(out), *srcs]
     if verbose_ptxas:
         cmd.insert(1, "-Xptxas=-v")

@@ -1,8 +1,556 @@
+// Attention backward on sm_100a (reference flash_bwd, core/src/flash_bwd.cpp:29-126).
+//
+//   K2 fa3b_bwd_prep_kernel   D = rowsum(dO o O) (bwd_preprocess, :29-41), the LSE in
+//                             log2 units, both padded to a multiple of 128 rows with
+//                             D = 0, LSE2 = +inf (so padded query columns get P = 0)
+//   K3 fa3b_bwd_kernel        KV-outer / Q-inner main loop (:58-110), one CTA per
+//                             (128-row KV tile, KV head, batch); the Q tiles of every
+//                             query head in the GQA group stream through it
+//   K4 fa3b_bwd_dq_kernel     dQ = alpha * dQaccum -> 16-bit (the alpha fold, :121-124)
+//
+// K3 computes the transposed scores so KV rows are TMEM lanes:
+//   S^T  = K Q^T      (tcgen05 SS, TMEM cols [0,128))
+//   dP^T = V dO^T     (tcgen05 SS, TMEM cols [128,256))
+//   P^T  = exp2(S^T * |alpha| log2e - LSE2), dS^T = P^T o (dP^T - D)   (2 warpgroups)
+//   dV  += P^T dO     (tcgen05 TS: P^T as 16-bit pairs in TMEM over the S^T columns)
+//   dK  += dS^T Q     (tcgen05 TS: dS^T over the dP^T columns)
+//   dQ_i = dS K       (tcgen05 SS: dS staged in shared memory, MN-major A)
+// dV and dK stay in TMEM for the whole CTA; dQ_i is drained by the softmax
+// warpgroups with red.global.add.v4.f32 into an fp32 workspace (the dQ-writer
+// role). The reference's deterministic ascending-j dQ order
+// is not kept (atomics); results equal it within rounding.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <mutex>
+
+#include "../../include/fa3b.h"
 #include "fa3b_internal.cuh"
-namespace fa3b { int launch_fwd_fp8(const fa3b_fwd_params&, cudaStream_t) { return FA3B_ERR_DTYPE; } }
-extern "C" {
-int fa3b_fp8_prepare(const fa3b_fp8_prepare_params*) { return FA3B_ERR_DTYPE; }
-int fa3b_bwd_preprocess(const fa3b_bwd_preprocess_params*) { return FA3B_ERR_DTYPE; }
-int fa3b_bwd(const fa3b_bwd_params*) { return FA3B_ERR_DTYPE; }
-size_t fa3b_bwd_workspace_bytes(int32_t, int32_t, int32_t, int32_t, int32_t) { return 0; }
+#include "sm100_ptx.cuh"
+
+namespace fa3b {
+
+namespace {
+
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ float load_elem(const void* p, size_t i, int dtype) {
+  if (dtype == FA3B_DTYPE_BF16) return __bfloat162float(static_cast<const __nv_bfloat16*>(p)[i]);
+  if (dtype == FA3B_DTYPE_F16) return __half2float(static_cast<const __half*>(p)[i]);
+  return static_cast<const float*>(p)[i];
 }
+
+// One warp per row: D_i = sum_j dO_ij O_ij (fp32 accumulate), optional LSE2.
+__global__ void fa3b_bwd_prep_kernel(const void* __restrict__ o, long long o_sb, long long o_ss,
+                                     long long o_sh, const void* __restrict__ dout,
+                                     long long d_sb, long long d_ss, long long d_sh, int dtype,
+                                     int N, int H, int D, int n_out, float* __restrict__ delta,
+                                     const float* __restrict__ lse, float* __restrict__ lse2) {
+  const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int lane = threadIdx.x & 31;
+  if (row >= n_out) return;
+  float acc = 0.f;
+  if (row < N) {
+    const size_t ob = b * o_sb + static_cast<size_t>(row) * o_ss + h * o_sh;
+    const size_t db = b * d_sb + static_cast<size_t>(row) * d_ss + h * d_sh;
+    for (int c = lane; c < D; c += 32) acc += load_elem(dout, db + c, dtype) * load_elem(o, ob + c, dtype);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0) {
+    const size_t idx = (static_cast<size_t>(b) * H + h) * n_out + row;
+    delta[idx] = acc;
+    if (lse2 != nullptr) {
+      float l = row < N ? lse[(static_cast<size_t>(b) * H + h) * N + row] : -INFINITY;
+      // rows that saw no key (L = -inf) and padding rows must get P = 0
+      lse2[idx] = (l == -INFINITY) ? INFINITY : l * kLog2e;
+    }
+  }
+}
+
+__global__ void fa3b_bwd_dq_kernel(const float* __restrict__ dq_acc, int Npad, int N, int H,
+                                   int D, float alpha, void* __restrict__ dq, long long q_sb,
+                                   long long q_ss, long long q_sh, int bf16) {
+  // one thread per 8 consecutive elements of a row
+  const int per_row = D / 8;
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<long long>(H) * N * per_row) return;
+  const int b = blockIdx.y;
+  const int c8 = static_cast<int>(idx % per_row);
+  const long long rh = idx / per_row;
+  const int row = static_cast<int>(rh % N);
+  const int h = static_cast<int>(rh / N);
+  const float4* src = reinterpret_cast<const float4*>(
+      dq_acc + ((static_cast<size_t>(b) * H + h) * Npad + row) * D + c8 * 8);
+  const float4 a = src[0], c = src[1];
+  uint4 out;
+  if (bf16) {
+    out = make_uint4(ptx::pack_bf16(a.x * alpha, a.y * alpha), ptx::pack_bf16(a.z * alpha, a.w * alpha),
+                     ptx::pack_bf16(c.x * alpha, c.y * alpha), ptx::pack_bf16(c.z * alpha, c.w * alpha));
+  } else {
+    out = make_uint4(ptx::pack_f16(a.x * alpha, a.y * alpha), ptx::pack_f16(a.z * alpha, a.w * alpha),
+                     ptx::pack_f16(c.x * alpha, c.y * alpha), ptx::pack_f16(c.z * alpha, c.w * alpha));
+  }
+  *reinterpret_cast<uint4*>(static_cast<uint16_t*>(dq) + b * q_sb + static_cast<size_t>(row) * q_ss +
+                            h * q_sh + c8 * 8) = out;
+}
+
+__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b),
+               "f"(c), "f"(d)
+               : "memory");
+}
+
+struct BwdArgs {
+  int B, H, Hkv, N, Npad, group;
+  float scale_log2;  // |alpha| log2e
+  float alpha;
+  const float* lse2;   // [B, H, Npad]
+  const float* delta;  // [B, H, Npad]
+  float* dq_acc;       // [B, H, Npad, D]
+  void* dk;
+  long long dk_sb, dk_ss, dk_sh;
+  void* dv;
+  long long dv_sb, dv_ss, dv_sh;
+};
+
+template <int D_>
+struct BwdTraits {
+  static constexpr int D = D_;
+  static constexpr int CHUNK_BYTES = 128 * 128;
+  static constexpr int TILE_BYTES = (D / 64) * CHUNK_BYTES;  // 128 rows x D 16-bit
+  static constexpr int NUM_THREADS = 256 + 64;
+  static constexpr int LOAD_WARP = 8;
+  static constexpr int MMA_WARP = 9;
+  static constexpr int OFF_K = 0;
+  static constexpr int OFF_V = TILE_BYTES;
+  static constexpr int OFF_Q = 2 * TILE_BYTES;          // 2 stages
+  static constexpr int OFF_DO = 4 * TILE_BYTES;         // 2 stages
+  static constexpr int OFF_DS = 6 * TILE_BYTES;         // 128 x 128 16-bit, MN-major
+  static constexpr int OFF_BAR = OFF_DS + 2 * CHUNK_BYTES;
+  // kv_full, q_full[2], q_empty[2], s_full, p_full, dq_full, dq_empty, dkv_full
+  static constexpr int NUM_BARS = 10;
+  static constexpr int SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16 + 1024;
+  static constexpr int COL_S = 0, COL_DP = 128, COL_DV = 256, COL_DK = 256 + D;
+  static constexpr bool ALIAS_DQ = (COL_DK + D + D > 512);
+  static constexpr int COL_DQ = ALIAS_DQ ? 0 : COL_DK + D;
+  static_assert(SMEM_BYTES <= 232448, "shared memory budget");
+};
+
+// TMEM column of the 16-bit P^T / dS^T pairs for K step t (16 query columns):
+// warpgroup w wrote its 64 columns as 32 packed columns at offset 64 w.
+__device__ __forceinline__ uint32_t pair_col(int t) { return (t >> 2) * 64 + (t & 3) * 8; }
+
+template <int D, bool CAUSAL, bool BF16>
+__global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
+    fa3b_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
+                    const BwdArgs args, const uint32_t idesc_s, const uint32_t idesc_dp,
+                    const uint32_t idesc_acc, const uint32_t idesc_dq) {
+  using T = BwdTraits<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + T::OFF_BAR);
+  uint64_t* kv_full = bars;
+  uint64_t* q_full = bars + 1;
+  uint64_t* q_empty = bars + 3;
+  uint64_t* s_full = bars + 5;
+  uint64_t* p_full = bars + 6;
+  uint64_t* dq_full = bars + 7;
+  uint64_t* dq_empty = bars + 8;
+  uint64_t* dkv_full = bars + 9;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + T::NUM_BARS);
+
+  const int warp = static_cast<int>(ptx::warp_id());
+  const int j = blockIdx.x;  // KV tile
+  const int hkv = blockIdx.y;
+  const int b = blockIdx.z;
+  const int N = args.N;
+  const int nq = (N + 127) / 128;
+  const int i0 = CAUSAL ? j : 0;
+  const int per_head = nq - i0;
+  const int n_iter = per_head * args.group;
+
+  if (warp == T::MMA_WARP) {
+    if (ptx::lane_id() == 0) {
+      ptx::mbar_init(kv_full, 1);
+      for (int s = 0; s < 2; ++s) {
+        ptx::mbar_init(&q_full[s], 1);
+        ptx::mbar_init(&q_empty[s], 1);
+      }
+      ptx::mbar_init(s_full, 1);
+      ptx::mbar_init(p_full, 256);
+      ptx::mbar_init(dq_full, 1);
+      ptx::mbar_init(dq_empty, 256);
+      ptx::mbar_init(dkv_full, 1);
+      ptx::fence_mbar_init();
+    }
+    __syncwarp();
+    ptx::tmem_alloc<512>(tmem_slot);
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == T::LOAD_WARP) {
+    if (ptx::elect_one()) {
+      ptx::prefetch_tmap(&tmQ);
+      ptx::prefetch_tmap(&tmK);
+      ptx::prefetch_tmap(&tmV);
+      ptx::prefetch_tmap(&tmdO);
+      ptx::mbar_arrive_expect_tx(kv_full, 2 * T::TILE_BYTES);
+      for (int c = 0; c < D / 64; ++c) {
+        ptx::tma_load_4d(smem + T::OFF_K + c * T::CHUNK_BYTES, &tmK, kv_full, c * 64, hkv, j * 128,
+                         b, ptx::kEvictNormal);
+        ptx::tma_load_4d(smem + T::OFF_V + c * T::CHUNK_BYTES, &tmV, kv_full, c * 64, hkv, j * 128,
+                         b, ptx::kEvictNormal);
+      }
+      for (int it = 0; it < n_iter; ++it) {
+        const int s = it & 1;
+        const int h = hkv * args.group + it / per_head;
+        const int i = i0 + it % per_head;
+        ptx::mbar_wait(&q_empty[s], ((it >> 1) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(&q_full[s], 2 * T::TILE_BYTES);
+        for (int c = 0; c < D / 64; ++c) {
+          ptx::tma_load_4d(smem + T::OFF_Q + s * T::TILE_BYTES + c * T::CHUNK_BYTES, &tmQ,
+                           &q_full[s], c * 64, h, i * 128, b, ptx::kEvictLast);
+          ptx::tma_load_4d(smem + T::OFF_DO + s * T::TILE_BYTES + c * T::CHUNK_BYTES, &tmdO,
+                           &q_full[s], c * 64, h, i * 128, b, ptx::kEvictLast);
+        }
+      }
+    }
+  } else if (warp == T::MMA_WARP) {
+    if (ptx::elect_one()) {
+      const uint32_t k_addr = ptx::smem_u32(smem + T::OFF_K);
+      const uint32_t v_addr = ptx::smem_u32(smem + T::OFF_V);
+      const uint32_t ds_addr = ptx::smem_u32(smem + T::OFF_DS);
+      ptx::mbar_wait(kv_full, 0);
+      for (int it = 0; it < n_iter; ++it) {
+        const int s = it & 1;
+        const uint32_t q_addr = ptx::smem_u32(smem + T::OFF_Q + s * T::TILE_BYTES);
+        const uint32_t do_addr = ptx::smem_u32(smem + T::OFF_DO + s * T::TILE_BYTES);
+        ptx::mbar_wait(&q_full[s], (it >> 1) & 1);
+        if (T::ALIAS_DQ && it > 0) ptx::mbar_wait(dq_empty, (it - 1) & 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {  // S^T = K Q^T, dP^T = V dO^T (K-major, SW128)
+          const uint32_t off = (k >> 2) * T::CHUNK_BYTES + (k & 3) * 32;
+          ptx::mma_f16_ss(tmem + T::COL_S, ptx::sw128_desc(k_addr + off, 16, 1024),
+                          ptx::sw128_desc(q_addr + off, 16, 1024), idesc_s, k > 0);
+          ptx::mma_f16_ss(tmem + T::COL_DP, ptx::sw128_desc(v_addr + off, 16, 1024),
+                          ptx::sw128_desc(do_addr + off, 16, 1024), idesc_dp, k > 0);
+        }
+        ptx::mma_commit(s_full);
+        ptx::mbar_wait(p_full, it & 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {  // dV += P^T dO, dK += dS^T Q (B MN-major)
+          const uint32_t boff = t * 16 * 128;
+          ptx::mma_f16_ts(tmem + T::COL_DV, tmem + T::COL_S + pair_col(t),
+                          ptx::sw128_desc(do_addr + boff, T::CHUNK_BYTES, 1024), idesc_acc,
+                          (it > 0 || t > 0));
+          ptx::mma_f16_ts(tmem + T::COL_DK, tmem + T::COL_DP + pair_col(t),
+                          ptx::sw128_desc(q_addr + boff, T::CHUNK_BYTES, 1024), idesc_acc,
+                          (it > 0 || t > 0));
+        }
+        if (!T::ALIAS_DQ && it > 0) {
+          ptx::mbar_wait(dq_empty, (it - 1) & 1);
+          ptx::tc_fence_after();
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {  // dQ_i = dS K (A and B MN-major)
+          const uint32_t off = t * 16 * 128;
+          ptx::mma_f16_ss(tmem + T::COL_DQ, ptx::sw128_desc(ds_addr + off, T::CHUNK_BYTES, 1024),
+                          ptx::sw128_desc(k_addr + off, T::CHUNK_BYTES, 1024), idesc_dq, t > 0);
+        }
+        ptx::mma_commit(dq_full);
+        ptx::mma_commit(&q_empty[s]);
+      }
+      ptx::mma_commit(dkv_full);
+    }
+  } else {
+    // ------------------------------------------------ 2 softmax/gradient warpgroups
+    const int w = warp >> 2;          // which 64-column half
+    const int r = threadIdx.x & 127;  // KV row in the tile == TMEM lane
+    const uint32_t lane_base = static_cast<uint32_t>(32 * (warp & 3)) << 16;
+    const int kv_row = j * 128 + r;
+    const float sl2 = args.scale_log2;
+    uint8_t* ds_row = smem + T::OFF_DS + w * T::CHUNK_BYTES + r * 128;
+    for (int it = 0; it < n_iter; ++it) {
+      const int h = hkv * args.group + it / per_head;
+      const int i = i0 + it % per_head;
+      const int q0 = i * 128 + 64 * w;
+      const size_t hb = static_cast<size_t>(b) * args.H + h;
+      const float4* lse4 = reinterpret_cast<const float4*>(args.lse2 + hb * args.Npad + q0);
+      const float4* del4 = reinterpret_cast<const float4*>(args.delta + hb * args.Npad + q0);
+      ptx::mbar_wait(s_full, it & 1);
+      ptx::tc_fence_after();
+      uint32_t sr[64], dpr[64];
+      ptx::tmem_ld32(tmem + lane_base + T::COL_S + 64 * w, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+      ptx::tmem_ld32(tmem + lane_base + T::COL_S + 64 * w + 32,
+                     *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+      ptx::tmem_ld32(tmem + lane_base + T::COL_DP + 64 * w,
+                     *reinterpret_cast<uint32_t(*)[32]>(&dpr[0]));
+      ptx::tmem_ld32(tmem + lane_base + T::COL_DP + 64 * w + 32,
+                     *reinterpret_cast<uint32_t(*)[32]>(&dpr[32]));
+      ptx::tmem_wait_ld();
+      const bool diag = CAUSAL && i == j;
+      uint32_t pk[32], dk2[32];
+#pragma unroll
+      for (int c4 = 0; c4 < 16; ++c4) {
+        const float4 l4 = __ldg(lse4 + c4);
+        const float4 d4 = __ldg(del4 + c4);
+        const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+        const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
+        float p[4], ds[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int c = c4 * 4 + e;
+          float pv = ptx::ex2(fmaf(__uint_as_float(sr[c]), sl2, -lv[e]));
+          if (diag && kv_row > q0 + c) pv = 0.f;
+          p[e] = pv;
+          ds[e] = pv * (__uint_as_float(dpr[c]) - dv[e]);
+        }
+        if (BF16) {
+          pk[2 * c4] = ptx::pack_bf16(p[0], p[1]);
+          pk[2 * c4 + 1] = ptx::pack_bf16(p[2], p[3]);
+          dk2[2 * c4] = ptx::pack_bf16(ds[0], ds[1]);
+          dk2[2 * c4 + 1] = ptx::pack_bf16(ds[2], ds[3]);
+        } else {
+          pk[2 * c4] = ptx::pack_f16(p[0], p[1]);
+          pk[2 * c4 + 1] = ptx::pack_f16(p[2], p[3]);
+          dk2[2 * c4] = ptx::pack_f16(ds[0], ds[1]);
+          dk2[2 * c4 + 1] = ptx::pack_f16(ds[2], ds[3]);
+        }
+      }
+      ptx::tmem_st32(tmem + lane_base + T::COL_S + 64 * w, pk);
+      ptx::tmem_st32(tmem + lane_base + T::COL_DP + 64 * w, dk2);
+      // dS (KV row r, 64 query columns) into the 128B-swizzled MN-major tile
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        *reinterpret_cast<uint4*>(ds_row + ((u ^ (r & 7)) << 4)) =
+            make_uint4(dk2[4 * u], dk2[4 * u + 1], dk2[4 * u + 2], dk2[4 * u + 3]);
+      }
+      ptx::fence_proxy_async_smem();
+      ptx::tmem_wait_st();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(p_full);
+
+      // drain dQ_i (TMEM lane = query row r of tile i) into the fp32 workspace
+      ptx::mbar_wait(dq_full, it & 1);
+      ptx::tc_fence_after();
+      float* dst = args.dq_acc + (hb * args.Npad + i * 128 + r) * D + w * (D / 2);
+      constexpr int NCH = D / 64;  // 32-column chunks per warpgroup half
+      uint32_t qv[NCH][32];
+#pragma unroll
+      for (int c = 0; c < NCH; ++c)
+        ptx::tmem_ld32(tmem + lane_base + T::COL_DQ + w * (D / 2) + c * 32, qv[c]);
+      ptx::tmem_wait_ld();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(dq_empty);
+#pragma unroll
+      for (int c = 0; c < NCH; ++c)
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          red_add_v4(dst + c * 32 + 4 * e, __uint_as_float(qv[c][4 * e]),
+                     __uint_as_float(qv[c][4 * e + 1]), __uint_as_float(qv[c][4 * e + 2]),
+                     __uint_as_float(qv[c][4 * e + 3]));
+    }
+    // ------------------------------------------------ epilogue: dK, dV
+    ptx::mbar_wait(dkv_full, 0);
+    ptx::tc_fence_after();
+    const bool row_ok = kv_row < N;
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {
+      const uint32_t col = (which ? T::COL_DK : T::COL_DV) + w * (D / 2);
+      const float scale = which ? args.alpha : 1.f;
+      uint16_t* base = static_cast<uint16_t*>(which ? args.dk : args.dv);
+      const size_t off = which ? (b * args.dk_sb + static_cast<size_t>(kv_row) * args.dk_ss + hkv * args.dk_sh)
+                               : (b * args.dv_sb + static_cast<size_t>(kv_row) * args.dv_ss + hkv * args.dv_sh);
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c) {
+        uint32_t v[32];
+        ptx::tmem_ld32(tmem + lane_base + col + c * 32, v);
+        ptx::tmem_wait_ld();
+        if (!row_ok) continue;
+        uint32_t pk2[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const float a0 = __uint_as_float(v[2 * e]) * scale, a1 = __uint_as_float(v[2 * e + 1]) * scale;
+          pk2[e] = BF16 ? ptx::pack_bf16(a0, a1) : ptx::pack_f16(a0, a1);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(base + off + w * (D / 2) + c * 32);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) dst[e] = make_uint4(pk2[4 * e], pk2[4 * e + 1], pk2[4 * e + 2], pk2[4 * e + 3]);
+      }
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == T::MMA_WARP) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem);
+  }
+}
+
+size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+
+struct Workspace {
+  float* dq_acc;
+  float* lse2;
+  float* delta;
+  size_t bytes;
+};
+
+Workspace carve(void* base, int B, int H, int Npad, int D) {
+  Workspace w{};
+  const size_t dq = align256(static_cast<size_t>(B) * H * Npad * D * 4);
+  const size_t vec = align256(static_cast<size_t>(B) * H * Npad * 4);
+  uint8_t* p = static_cast<uint8_t*>(base);
+  w.dq_acc = reinterpret_cast<float*>(p);
+  w.lse2 = reinterpret_cast<float*>(p + dq);
+  w.delta = reinterpret_cast<float*>(p + dq + vec);
+  w.bytes = dq + 2 * vec;
+  return w;
+}
+
+template <int D, bool CAUSAL, bool BF16>
+int launch_bwd_main(const fa3b_bwd_params& p, const Workspace& ws, int Npad, cudaStream_t st) {
+  using Tr = BwdTraits<D>;
+  auto kern = fa3b_bwd_kernel<D, CAUSAL, BF16>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Tr::SMEM_BYTES);
+  });
+  if (attr_err != cudaSuccess) return cuda_fail(attr_err);
+  CUtensorMap tq, tk, tv, tdo;
+  int rc;
+  if ((rc = make_tmap_4d(&tq, p.q, 2, D, p.heads_q, p.seqlen, p.batch, 64, 128)) != FA3B_OK) return rc;
+  if ((rc = make_tmap_4d(&tk, p.k, 2, D, p.heads_kv, p.seqlen, p.batch, 64, 128)) != FA3B_OK) return rc;
+  if ((rc = make_tmap_4d(&tv, p.v, 2, D, p.heads_kv, p.seqlen, p.batch, 64, 128)) != FA3B_OK) return rc;
+  if ((rc = make_tmap_4d(&tdo, p.dout, 2, D, p.heads_q, p.seqlen, p.batch, 64, 128)) != FA3B_OK) return rc;
+  BwdArgs a;
+  a.B = p.batch;
+  a.H = p.heads_q;
+  a.Hkv = p.heads_kv;
+  a.N = p.seqlen;
+  a.Npad = Npad;
+  a.group = p.heads_q / p.heads_kv;
+  a.scale_log2 = static_cast<float>(std::fabs(p.alpha) * 1.4426950408889634);
+  a.alpha = static_cast<float>(p.alpha);
+  a.lse2 = ws.lse2;
+  a.delta = ws.delta;
+  a.dq_acc = ws.dq_acc;
+  a.dk = p.dk.ptr;
+  a.dk_sb = p.dk.stride_batch;
+  a.dk_ss = p.dk.stride_seq;
+  a.dk_sh = p.dk.stride_head;
+  a.dv = p.dv.ptr;
+  a.dv_sb = p.dv.stride_batch;
+  a.dv_ss = p.dv.stride_seq;
+  a.dv_sh = p.dv.stride_head;
+  const uint32_t fmt = BF16 ? 1u : 0u;
+  const uint32_t idesc_s = ptx::make_idesc(128, 128, fmt, fmt, false, false, p.alpha < 0);
+  const uint32_t idesc_dp = ptx::make_idesc(128, 128, fmt, fmt, false, false, false);
+  const uint32_t idesc_acc = ptx::make_idesc(128, D, fmt, fmt, false, true, false);
+  const uint32_t idesc_dq = ptx::make_idesc(128, D, fmt, fmt, true, true, false);
+  dim3 grid(Npad / 128, p.heads_kv, p.batch);
+  kern<<<grid, Tr::NUM_THREADS, Tr::SMEM_BYTES, st>>>(tq, tk, tv, tdo, a, idesc_s, idesc_dp, idesc_acc,
+                                                      idesc_dq);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? FA3B_OK : cuda_fail(e);
+}
+
+template <int D>
+int launch_bwd_main_dt(const fa3b_bwd_params& p, const Workspace& ws, int Npad, cudaStream_t st) {
+  const bool bf16 = p.dtype == FA3B_DTYPE_BF16;
+  if (p.causal) return bf16 ? launch_bwd_main<D, true, true>(p, ws, Npad, st) : launch_bwd_main<D, true, false>(p, ws, Npad, st);
+  return bf16 ? launch_bwd_main<D, false, true>(p, ws, Npad, st) : launch_bwd_main<D, false, false>(p, ws, Npad, st);
+}
+
+int launch_prep(const fa3b_tensor4& o, const fa3b_tensor4& dout, int dtype, int B, int H, int N, int D,
+                int n_out, float* delta, const float* lse, float* lse2, cudaStream_t st) {
+  dim3 grid((n_out + 7) / 8, H, B);
+  fa3b_bwd_prep_kernel<<<grid, 256, 0, st>>>(o.ptr, o.stride_batch, o.stride_seq, o.stride_head, dout.ptr,
+                                            dout.stride_batch, dout.stride_seq, dout.stride_head, dtype, N,
+                                            H, D, n_out, delta, lse, lse2);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? FA3B_OK : cuda_fail(e);
+}
+
+}  // namespace
+}  // namespace fa3b
+
+using namespace fa3b;
+
+extern "C" {
+
+size_t fa3b_bwd_workspace_bytes(int32_t batch, int32_t heads_q, int32_t heads_kv, int32_t seqlen,
+                                int32_t head_dim) {
+  (void)heads_kv;
+  if (batch <= 0 || heads_q <= 0 || seqlen <= 0 || head_dim <= 0) return 0;
+  const int Npad = (seqlen + 127) / 128 * 128;
+  return carve(nullptr, batch, heads_q, Npad, head_dim).bytes;
+}
+
+int fa3b_bwd_preprocess(const fa3b_bwd_preprocess_params* pp) {
+  g_last_launch_count = 0;
+  if (pp == nullptr) return FA3B_ERR_NULL;
+  if (pp->struct_size != sizeof(fa3b_bwd_preprocess_params)) return FA3B_ERR_STRUCT;
+  const auto& p = *pp;
+  if (p.batch <= 0 || p.heads <= 0 || p.seqlen <= 0 || p.head_dim <= 0) return FA3B_ERR_EMPTY;
+  if (!p.o.ptr || !p.dout.ptr || !p.delta) return FA3B_ERR_NULL;
+  if (p.dtype != FA3B_DTYPE_BF16 && p.dtype != FA3B_DTYPE_F16 && p.dtype != FA3B_DTYPE_F32)
+    return FA3B_ERR_DTYPE;
+  int rc = launch_prep(p.o, p.dout, p.dtype, p.batch, p.heads, p.seqlen, p.head_dim, p.seqlen, p.delta,
+                       nullptr, nullptr, static_cast<cudaStream_t>(p.stream));
+  if (rc == FA3B_OK) g_last_launch_count = 1;
+  return rc;
+}
+
+int fa3b_bwd(const fa3b_bwd_params* pp) {
+  g_last_launch_count = 0;
+  if (pp == nullptr) return FA3B_ERR_NULL;
+  if (pp->struct_size != sizeof(fa3b_bwd_params)) return FA3B_ERR_STRUCT;
+  const auto& p = *pp;
+  int rc = validate_problem(p.batch, p.heads_q, p.heads_kv, p.seqlen, p.head_dim, p.alpha);
+  if (rc != FA3B_OK) return rc;
+  if (p.head_dim == 256) return FA3B_ERR_HEAD_DIM;  // dK + dV alone fill TMEM
+  if (p.dtype != FA3B_DTYPE_BF16 && p.dtype != FA3B_DTYPE_F16) return FA3B_ERR_DTYPE;
+  if (!p.q.ptr || !p.k.ptr || !p.v.ptr || !p.o.ptr || !p.dout.ptr || !p.dq.ptr || !p.dk.ptr ||
+      !p.dv.ptr || !p.lse)
+    return FA3B_ERR_NULL;
+  const int B = p.batch, H = p.heads_q, Hkv = p.heads_kv, N = p.seqlen, D = p.head_dim;
+  if (!strides_ok(p.q, 2, B, N, H) || !strides_ok(p.k, 2, B, N, Hkv) || !strides_ok(p.v, 2, B, N, Hkv) ||
+      !strides_ok(p.o, 2, B, N, H) || !strides_ok(p.dout, 2, B, N, H) || !strides_ok(p.dq, 2, B, N, H) ||
+      !strides_ok(p.dk, 2, B, N, Hkv) || !strides_ok(p.dv, 2, B, N, Hkv))
+    return FA3B_ERR_ALIGNMENT;
+  const int Npad = (N + 127) / 128 * 128;
+  const Workspace ws = carve(p.workspace, B, H, Npad, D);
+  if (p.workspace == nullptr || p.workspace_bytes < ws.bytes || !aligned16(p.workspace))
+    return FA3B_ERR_WORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(p.stream);
+  cudaError_t e = cudaMemsetAsync(ws.dq_acc, 0, static_cast<size_t>(B) * H * Npad * D * 4, st);
+  if (e != cudaSuccess) return cuda_fail(e);
+  if ((rc = launch_prep(p.o, p.dout, p.dtype, B, H, N, D, Npad, ws.delta, p.lse, ws.lse2, st)) != FA3B_OK)
+    return rc;
+  rc = D == 64 ? launch_bwd_main_dt<64>(p, ws, Npad, st) : launch_bwd_main_dt<128>(p, ws, Npad, st);
+  if (rc != FA3B_OK) return rc;
+  const long long per_b = static_cast<long long>(H) * N * (D / 8);
+  dim3 grid(static_cast<unsigned>((per_b + 255) / 256), B);
+  fa3b_bwd_dq_kernel<<<grid, 256, 0, st>>>(ws.dq_acc, Npad, N, H, D, static_cast<float>(p.alpha), p.dq.ptr,
+                                           p.dq.stride_batch, p.dq.stride_seq, p.dq.stride_head,
+                                           p.dtype == FA3B_DTYPE_BF16);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e);
+  g_last_launch_count = 4;  // memset + prep + main + dq convert
+  return FA3B_OK;
+}
+
+}  // extern "C"
