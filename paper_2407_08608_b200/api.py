@@ -63,8 +63,8 @@ def fwd(q, k, v, *, causal: bool = False, alpha: float | None = None,
     p.causal = int(bool(causal))
     p.schedule = _SCHED[schedule]
     p.q_scale, p.k_scale, p.v_scale = _ptr(q_scale), _ptr(k_scale), _ptr(v_scale)
-    p.q_block_rows = q_block_rows if q_scale is not None else 0
-    p.kv_block_rows = kv_block_rows if k_scale is not None else 0
+    p.q_block_rows = q_block_rows
+    p.kv_block_rows = kv_block_rows
     p.stream = _stream(stream)
     _lib.check(_lib.load().fa3b_fwd(ctypes.byref(p)))
     return out, lse
@@ -94,6 +94,21 @@ def fp8_prepare(x, *, block_rows: int = 128, hadamard: bool = True, seed: int = 
     p.stream = _stream(stream)
     _lib.check(_lib.load().fa3b_fp8_prepare(ctypes.byref(p)))
     return out, scales
+
+
+def fp8_fwd(q, k, v, *, causal: bool = False, alpha: float | None = None,
+            per_block: bool = True, incoherent: bool = True, seed: int = 0,
+            schedule: str = "pingpong", out_dtype=None, stream=None):
+    """The reference's fp8_flash_fwd (fp8_attention.cpp:77-181) on the device:
+    K5 (Hadamard on Q and K with one seed, block or tensor quantization of Q,
+    K, V) then K6. Inputs are 16-bit or fp32 [B, N, H, D]; returns (O, LSE)."""
+    blk = 128 if per_block else 0
+    q8, sq = fp8_prepare(q, block_rows=blk, hadamard=incoherent, seed=seed, stream=stream)
+    k8, sk = fp8_prepare(k, block_rows=blk, hadamard=incoherent, seed=seed, stream=stream)
+    v8, sv = fp8_prepare(v, block_rows=blk, hadamard=False, stream=stream)
+    return fwd(q8, k8, v8, causal=causal, alpha=alpha, schedule=schedule, out_dtype=out_dtype,
+               q_scale=sq, k_scale=sk, v_scale=sv, q_block_rows=blk, kv_block_rows=blk,
+               stream=stream)
 
 
 def bwd_preprocess(o, dout, *, delta=None, stream=None):

@@ -111,7 +111,7 @@ namespace {
 template <int D, int NT, bool CAUSAL, bool BF16>
 int launch_fwd16(const fa3b_fwd_params& p, cudaStream_t stream) {
   using T = FwdTraits<D, NT>;
-  auto kern = fa3b_fwd_kernel<D, NT, CAUSAL, BF16>;
+  auto kern = fa3b_fwd_kernel<D, NT, CAUSAL, BF16 ? KIND_BF16 : KIND_F16>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
@@ -142,6 +142,9 @@ int launch_fwd16(const fa3b_fwd_params& p, cudaStream_t stream) {
   a.o_sh = p.o.stride_head;
   a.out_f32 = p.out_dtype == FA3B_DTYPE_F32;
   a.lse = p.lse;
+  a.q_scale = a.k_scale = a.v_scale = nullptr;
+  a.q_blocked = a.kv_blocked = 0;
+  a.fp8_thr = 8.f;
   const uint32_t fmt = BF16 ? 1u : 0u;
   const uint32_t idesc_qk = ptx::make_idesc(128, 128, fmt, fmt, false, false, p.alpha < 0);
   const uint32_t idesc_pv = ptx::make_idesc(128, D, fmt, fmt, false, true, false);

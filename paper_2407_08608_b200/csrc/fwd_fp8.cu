@@ -1,5 +1,94 @@
-// K6 placeholder until the FP8 forward lands.
+// K6 launcher: the FP8 (e4m3) forward, fa3b_fwd_kernel<..., KIND_E4M3>.
+// Replaces the main loop of fp8_flash_fwd (core/src/fp8_attention.cpp:99-178);
+// the operands come from K5 (fa3b_fp8_prepare). See fwd_kernel.cuh for the
+// scale handling.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdlib>
+#include <mutex>
+
 #include "fa3b_internal.cuh"
+#include "fwd_kernel.cuh"
+
 namespace fa3b {
-int launch_fwd_fp8(const fa3b_fwd_params&, cudaStream_t) { return FA3B_ERR_DTYPE; }
+namespace {
+
+// log2 headroom of the e4m3 P: codes = P * 448 / 2^thr with P <= 2^thr.
+// With per-block V scales O is rescaled every block anyway, so the running
+// max is kept exact (thr 0, P <= 1, the reference's P range); per tensor a
+// lazy max (thr 4) skips most O rescales. FA3B_FP8_THR overrides both.
+float fp8_threshold(bool kv_blocked) {
+  static const float env = [] {
+    const char* e = std::getenv("FA3B_FP8_THR");
+    const float v = e ? static_cast<float>(std::atof(e)) : -1.f;
+    return (v >= 0.f && v <= 8.f) ? v : -1.f;
+  }();
+  if (env >= 0.f) return env;
+  return kv_blocked ? 0.f : 4.f;
+}
+
+template <int D, int NT, bool CAUSAL>
+int launch(const fa3b_fwd_params& p, cudaStream_t stream) {
+  using T = FwdTraits<D, NT, 1>;
+  auto kern = fa3b_fwd_kernel<D, NT, CAUSAL, KIND_E4M3>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM_BYTES);
+  });
+  if (attr_err != cudaSuccess) return cuda_fail(attr_err);
+  CUtensorMap tq, tk, tv;
+  int rc;
+  if ((rc = make_tmap_4d(&tq, p.q, 1, D, p.heads_q, p.seqlen, p.batch, 128, 128)) != FA3B_OK) return rc;
+  if ((rc = make_tmap_4d(&tk, p.k, 1, D, p.heads_kv, p.seqlen, p.batch, 128, 128)) != FA3B_OK) return rc;
+  if ((rc = make_tmap_4d(&tv, p.v, 1, D, p.heads_kv, p.seqlen, p.batch, 128, 128)) != FA3B_OK) return rc;
+  FwdArgs a;
+  a.B = p.batch;
+  a.H = p.heads_q;
+  a.Hkv = p.heads_kv;
+  a.N = p.seqlen;
+  a.group = p.heads_q / p.heads_kv;
+  a.scale_log2 = static_cast<float>(std::fabs(p.alpha) * 1.4426950408889634);
+  a.o = p.o.ptr;
+  a.o_sb = p.o.stride_batch;
+  a.o_ss = p.o.stride_seq;
+  a.o_sh = p.o.stride_head;
+  a.out_f32 = p.out_dtype == FA3B_DTYPE_F32;
+  a.lse = p.lse;
+  a.q_scale = p.q_scale;
+  a.k_scale = p.k_scale;
+  a.v_scale = p.v_scale;
+  a.q_blocked = p.q_block_rows != 0;
+  a.kv_blocked = p.kv_block_rows != 0;
+  a.fp8_thr = fp8_threshold(a.kv_blocked != 0);
+  const uint32_t idesc_qk = ptx::make_idesc(128, 128, 0, 0, false, false, p.alpha < 0);
+  const uint32_t idesc_pv = ptx::make_idesc(128, D, 0, 0, false, true, false);
+  dim3 grid((p.seqlen + NT * 128 - 1) / (NT * 128), p.heads_q, p.batch);
+  kern<<<grid, T::NUM_THREADS, T::SMEM_BYTES, stream>>>(tq, tk, tv, a, idesc_qk, idesc_pv);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e);
+  g_last_launch_count = 1;
+  return FA3B_OK;
+}
+
+}  // namespace
+
+int launch_fwd_fp8(const fa3b_fwd_params& p, cudaStream_t s) {
+  if (!p.q_scale || !p.k_scale || !p.v_scale) return FA3B_ERR_NULL;
+  if ((p.q_block_rows != 0 && p.q_block_rows != 128) ||
+      (p.kv_block_rows != 0 && p.kv_block_rows != 128))
+    return FA3B_ERR_BLOCK;
+  const bool basic = p.schedule == FA3B_SCHED_BASIC;
+  switch (p.head_dim) {
+    case 128:
+      if (p.causal) return basic ? launch<128, 1, true>(p, s) : launch<128, 2, true>(p, s);
+      return basic ? launch<128, 1, false>(p, s) : launch<128, 2, false>(p, s);
+    case 256:
+      return p.causal ? launch<256, 1, true>(p, s) : launch<256, 1, false>(p, s);
+  }
+  return FA3B_ERR_HEAD_DIM;  // e4m3 rows of 64 bytes would need a 64B swizzle
+}
+
 }  // namespace fa3b

@@ -23,14 +23,29 @@
 // and vice versa (the paper's inter-warpgroup ping-pong).
 //
 // The running max is kept lazily: O and l are only rescaled when the block
-// max exceeds the max in use by more than 2^8 (log2 domain), so P <= 256.
-// The result equals the reference's rescale-every-block arithmetic up to
-// rounding (flash_fwd.cpp:36-45).
+// max exceeds the max in use by more than 2^THR (log2 domain), so P <= 2^THR
+// (THR = 8 for 16-bit P). The result equals the reference's
+// rescale-every-block arithmetic up to rounding (flash_fwd.cpp:36-45).
+//
+// KIND = E4M3 is the FP8 forward K6 (fp8_flash_fwd, core/src/fp8_attention.cpp:
+// 77-181): Q/K/V are e4m3 codes with per-128-row-block (or per-tensor) scales
+// from K5; the S descale alpha s_q s_k[j] folds into the exp2 pre-scale
+// (PAPER.md:605-606); P is requantized to e4m3 with the fixed scale 2^THR/448
+// (THR = args.fp8_thr) instead of the reference's per-block amax, which is
+// ~1 for every block (proj/README.md:116-121). V's per-block scale is applied
+// exactly, as the reference does to each PV product (fp8_attention.cpp:158-164):
+// O is kept in units of the current block's s_v, i.e. rescaled by
+// s_v[j-1] / s_v[j] in the same TMEM pass as the softmax rescale, and the last
+// s_v is applied in the epilogue. (Folding s_v into P instead costs ~15% RMSE
+// on outlier inputs because small P codes drop into e4m3 subnormals.) Both MMAs run as tcgen05 kind::f8f6f4 with V consumed
+// MN-major straight from the TMA tile (no in-kernel transpose on sm_100a).
 #pragma once
 
 #include "sm100_ptx.cuh"
 
 namespace fa3b {
+
+enum FwdKind { KIND_F16 = 0, KIND_BF16 = 1, KIND_E4M3 = 2 };
 
 struct FwdArgs {
   int B, H, Hkv, N;
@@ -40,18 +55,26 @@ struct FwdArgs {
   long long o_sb, o_ss, o_sh;  // element strides of O
   int out_f32;
   float* lse;         // [B, H, N] or nullptr
+  // E4M3 only
+  const float* q_scale;  // [B, H, nqb] (per 128-row block) or [B, H] (per tensor)
+  const float* k_scale;  // [B, Hkv, nkb] or [B, Hkv]
+  const float* v_scale;
+  int q_blocked, kv_blocked;
+  float fp8_thr;         // lazy-rescale threshold (log2) for the e4m3 P
 };
 
-template <int D_, int NT_>
+template <int D_, int NT_, int EB_ = 2>
 struct FwdTraits {
   static constexpr int D = D_;
   static constexpr int NT = NT_;
+  static constexpr int EB = EB_;  // bytes per element (2 f16/bf16, 1 e4m3)
   static constexpr int BM = 128;
   static constexpr int BN = 128;
-  static constexpr int CHUNK_BYTES = 128 * 128;  // 128 rows x 64 16-bit elements
-  static constexpr int CHUNKS = D / 64;
+  static constexpr int CHUNK_BYTES = 128 * 128;  // 128 rows x 128 bytes
+  static constexpr int CHUNK_ELEMS = 128 / EB;
+  static constexpr int CHUNKS = D / CHUNK_ELEMS;
   static constexpr int TILE_BYTES = CHUNKS * CHUNK_BYTES;
-  static constexpr int STAGES = D == 64 ? 8 : (D == 128 ? 4 : 2);
+  static constexpr int STAGES = TILE_BYTES <= 16384 ? 8 : (TILE_BYTES <= 32768 ? 4 : 2);
   static constexpr int NUM_THREADS = NT * 128 + 64;
   static constexpr int LOAD_WARP = NT * 4;
   static constexpr int MMA_WARP = NT * 4 + 1;
@@ -68,13 +91,15 @@ struct FwdTraits {
   __host__ __device__ static constexpr int o_col(int t) { return NT * 128 + t * D; }
 };
 
-template <int D, int NT, bool CAUSAL, bool BF16>
-__global__ void __launch_bounds__(FwdTraits<D, NT>::NUM_THREADS, 1)
+template <int D, int NT, bool CAUSAL, int KIND>
+__global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2>::NUM_THREADS, 1)
     fa3b_fwd_kernel(const __grid_constant__ CUtensorMap tmQ,
                     const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const FwdArgs args,
                     const uint32_t idesc_qk, const uint32_t idesc_pv) {
-  using T = FwdTraits<D, NT>;
+  constexpr bool FP8 = KIND == KIND_E4M3;
+  constexpr bool BF16 = KIND == KIND_BF16;
+  using T = FwdTraits<D, NT, FP8 ? 1 : 2>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -145,7 +170,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT>::NUM_THREADS, 1)
 #pragma unroll
         for (int c = 0; c < T::CHUNKS; ++c)
           ptx::tma_load_4d(smem + T::OFF_Q + t * T::TILE_BYTES + c * T::CHUNK_BYTES, &tmQ,
-                           q_full, c * 64, h, q_base + t * 128, b, ptx::kEvictFirst);
+                           q_full, c * T::CHUNK_ELEMS, h, q_base + t * 128, b, ptx::kEvictFirst);
       }
       int item = 0;
       for (int j = 0; j < n_max; ++j) {
@@ -158,8 +183,8 @@ __global__ void __launch_bounds__(FwdTraits<D, NT>::NUM_THREADS, 1)
           uint8_t* dst = smem + T::OFF_KV + slot * T::TILE_BYTES;
 #pragma unroll
           for (int c = 0; c < T::CHUNKS; ++c)
-            ptx::tma_load_4d(dst + c * T::CHUNK_BYTES, kv ? &tmV : &tmK, &kv_full[slot], c * 64,
-                             hkv, j * 128, b, ptx::kEvictLast);
+            ptx::tma_load_4d(dst + c * T::CHUNK_BYTES, kv ? &tmV : &tmK, &kv_full[slot],
+                             c * T::CHUNK_ELEMS, hkv, j * 128, b, ptx::kEvictLast);
         }
       }
     }
@@ -168,22 +193,33 @@ __global__ void __launch_bounds__(FwdTraits<D, NT>::NUM_THREADS, 1)
     if (ptx::elect_one()) {
       const uint32_t q_addr = ptx::smem_u32(smem + T::OFF_Q);
       const uint32_t kv_addr = ptx::smem_u32(smem + T::OFF_KV);
+      // one MMA consumes 32 bytes of K: 16 f16/bf16 or 32 e4m3 elements
+      constexpr int KSTEP = 32 / T::EB;
       auto issue_qk = [&](int t, int slot) {
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
+        for (int k = 0; k < D / KSTEP; ++k) {
           const uint32_t off = (k >> 2) * T::CHUNK_BYTES + (k & 3) * 32;
           const uint64_t a = ptx::sw128_desc(q_addr + t * T::TILE_BYTES + off, 16, 1024);
           const uint64_t bd = ptx::sw128_desc(kv_addr + slot * T::TILE_BYTES + off, 16, 1024);
-          ptx::mma_f16_ss(tmem + T::s_col(t), a, bd, idesc_qk, k > 0 ? 1u : 0u);
+          if constexpr (FP8)
+            ptx::mma_f8_ss(tmem + T::s_col(t), a, bd, idesc_qk, k > 0 ? 1u : 0u);
+          else
+            ptx::mma_f16_ss(tmem + T::s_col(t), a, bd, idesc_qk, k > 0 ? 1u : 0u);
         }
       };
       auto issue_pv = [&](int t, int slot, bool acc) {
 #pragma unroll
-        for (int k = 0; k < 128 / 16; ++k) {
-          const uint64_t bd = ptx::sw128_desc(kv_addr + slot * T::TILE_BYTES + k * 16 * 128,
+        for (int k = 0; k < 128 / KSTEP; ++k) {
+          // B = V, MN-major: KSTEP kv rows of 128 bytes per step
+          const uint64_t bd = ptx::sw128_desc(kv_addr + slot * T::TILE_BYTES + k * KSTEP * 128,
                                               T::CHUNK_BYTES, 1024);
-          ptx::mma_f16_ts(tmem + T::o_col(t), tmem + T::s_col(t) + k * 8, bd, idesc_pv,
-                          (acc || k > 0) ? 1u : 0u);
+          // A = P in TMEM: KSTEP elements = 8 columns of 32 bits
+          if constexpr (FP8)
+            ptx::mma_f8_ts(tmem + T::o_col(t), tmem + T::s_col(t) + k * 8, bd, idesc_pv,
+                           (acc || k > 0) ? 1u : 0u);
+          else
+            ptx::mma_f16_ts(tmem + T::o_col(t), tmem + T::s_col(t) + k * 8, bd, idesc_pv,
+                            (acc || k > 0) ? 1u : 0u);
         }
       };
       ptx::mbar_wait(q_full, 0);
@@ -233,11 +269,37 @@ __global__ void __launch_bounds__(FwdTraits<D, NT>::NUM_THREADS, 1)
     const uint32_t tS = tmem + lane_base + T::s_col(t);
     const uint32_t tO = tmem + lane_base + T::o_col(t);
     const int q_row = q_base + t * 128 + r;
-    const int nt = n_t[t];
-    const float sl2 = args.scale_log2;
+    const int nt = (t == 0) ? n_t[0] : n_t[NT - 1];
+    float sl2 = args.scale_log2;
+    float thr = 8.f;
+    float out_scale = 1.f;
+    const float* kscale = nullptr;
+    const float* vscale = nullptr;
+    if constexpr (FP8) {
+      const size_t hq = static_cast<size_t>(b) * args.H + h;
+      const size_t hk = static_cast<size_t>(b) * args.Hkv + hkv;
+      const int nqb_all = (N + 127) / 128;
+      sl2 *= args.q_blocked ? args.q_scale[hq * nqb_all + q_base / 128 + t] : args.q_scale[hq];
+      kscale = args.kv_blocked ? args.k_scale + hk * nkv : args.k_scale + hk;
+      vscale = args.kv_blocked ? args.v_scale + hk * nkv : args.v_scale + hk;
+      thr = args.fp8_thr;
+    }
+    float v_cur = 0.f;  // V scale the O accumulator is expressed in (FP8)
     float m_use = -INFINITY;  // running max in use, scaled log2 units
     float l = 0.f;
     for (int j = 0; j < nt; ++j) {
+      float slj = sl2;
+      float pmul = 1.f;
+      float vfac = 1.f;  // O rescale for a new V block scale (uniform across the CTA)
+      if constexpr (FP8) {
+        slj = sl2 * kscale[args.kv_blocked ? j : 0];
+        const float vs = vscale[args.kv_blocked ? j : 0];
+        if (vs != v_cur) {
+          vfac = v_cur / vs;  // 0 on the first block: O is empty
+          v_cur = vs;
+        }
+        pmul = 448.f * ptx::ex2(-thr);  // e4m3 codes of P: P * 448 / 2^thr
+      }
       ptx::mbar_wait(&s_full[t], j & 1);
       ptx::tc_fence_after();
       uint32_t sr[128];
@@ -258,34 +320,57 @@ __global__ void __launch_bounds__(FwdTraits<D, NT>::NUM_THREADS, 1)
       float mx = s[0];
 #pragma unroll
       for (int i = 1; i < 128; ++i) mx = fmaxf(mx, s[i]);
-      const float m_new = fmaxf(m_use, mx * sl2);
-      const bool resc = m_new > m_use + 8.f;
+      const float m_new = fmaxf(m_use, mx * slj);
+      const bool resc = m_new > m_use + thr;
       const float m_cur = resc ? m_new : m_use;
       const float factor = resc ? ptx::ex2(m_use - m_new) : 1.f;
       const float msub = (m_cur == -INFINITY) ? 0.f : m_cur;
       float sum0 = 0.f, sum1 = 0.f;
-      uint32_t pk[64];
+      if constexpr (FP8) {
+        uint32_t pk[32];
 #pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        const float p0 = ptx::ex2(fmaf(s[2 * i], sl2, -msub));
-        const float p1 = ptx::ex2(fmaf(s[2 * i + 1], sl2, -msub));
-        sum0 += p0;
-        sum1 += p1;
-        pk[i] = BF16 ? ptx::pack_bf16(p0, p1) : ptx::pack_f16(p0, p1);
+        for (int i = 0; i < 32; ++i) {
+          const float p0 = ptx::ex2(fmaf(s[4 * i], slj, -msub));
+          const float p1 = ptx::ex2(fmaf(s[4 * i + 1], slj, -msub));
+          const float p2 = ptx::ex2(fmaf(s[4 * i + 2], slj, -msub));
+          const float p3 = ptx::ex2(fmaf(s[4 * i + 3], slj, -msub));
+          sum0 += p0 + p2;
+          sum1 += p1 + p3;
+          pk[i] = ptx::pack_e4m3x4(p0 * pmul, p1 * pmul, p2 * pmul, p3 * pmul);
+        }
+        ptx::tmem_st32(tS, pk);
+      } else {
+        uint32_t pk[64];
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          const float p0 = ptx::ex2(fmaf(s[2 * i], slj, -msub));
+          const float p1 = ptx::ex2(fmaf(s[2 * i + 1], slj, -msub));
+          sum0 += p0;
+          sum1 += p1;
+          pk[i] = BF16 ? ptx::pack_bf16(p0, p1) : ptx::pack_f16(p0, p1);
+        }
+        ptx::tmem_st32(tS, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+        ptx::tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
       }
       l = l * factor + (sum0 + sum1);
-      ptx::tmem_st32(tS, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
-      ptx::tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
-      if (j > 0 && __any_sync(0xffffffffu, resc)) {
-        // PV(V_{j-1}) is complete (see header); rescale this row of O_t.
+      const float ofac = factor * vfac;
+      if (j > 0 && __any_sync(0xffffffffu, ofac != 1.f)) {
+        // PV(V_{j-1}) is complete (see header); rescale this row of O_t,
+        // up to 128 columns per batch of TMEM loads.
+        constexpr int G = D / 32 < 4 ? D / 32 : 4;
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t ov[32];
-          ptx::tmem_ld32(tO + c * 32, ov);
+        for (int c0 = 0; c0 < D / 32; c0 += G) {
+          uint32_t ov[G][32];
+#pragma unroll
+          for (int c = 0; c < G; ++c) ptx::tmem_ld32(tO + (c0 + c) * 32, ov[c]);
           ptx::tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * factor);
-          ptx::tmem_st32(tO + c * 32, ov);
+          for (int c = 0; c < G; ++c) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              ov[c][i] = __float_as_uint(__uint_as_float(ov[c][i]) * ofac);
+            ptx::tmem_st32(tO + (c0 + c) * 32, ov[c]);
+          }
         }
       }
       ptx::tmem_wait_st();
@@ -297,7 +382,8 @@ __global__ void __launch_bounds__(FwdTraits<D, NT>::NUM_THREADS, 1)
       // ---------------------------------------------------------- epilogue
       ptx::mbar_wait(&o_full[t], 0);
       ptx::tc_fence_after();
-      const float inv = l > 0.f ? 1.f / l : 0.f;
+      if constexpr (FP8) out_scale = v_cur * ptx::ex2(thr) * (1.f / 448.f);
+      const float inv = l > 0.f ? out_scale / l : 0.f;
       const bool row_ok = q_row < N;
       const size_t obase = static_cast<size_t>(b) * args.o_sb +
                            static_cast<size_t>(q_row) * args.o_ss +
@@ -322,7 +408,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT>::NUM_THREADS, 1)
           for (int i = 0; i < 16; ++i) {
             const float a = __uint_as_float(ov[2 * i]) * inv;
             const float bb = __uint_as_float(ov[2 * i + 1]) * inv;
-            pk[i] = BF16 ? ptx::pack_bf16(a, bb) : ptx::pack_f16(a, bb);
+            pk[i] = (BF16 || FP8) ? ptx::pack_bf16(a, bb) : ptx::pack_f16(a, bb);
           }
           uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(args.o) + obase + c * 32);
 #pragma unroll
