@@ -18,7 +18,8 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
-NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+NVCC = os.environ.get("NVCC", f"{CUDA_HOME}/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CUDA_SOURCES = ["fa3b_capi.cu", "fwd_fp8.cu", "fp8_prepare.cu", "bwd.cu"]
@@ -61,9 +62,10 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> Path:
     _run(cmd)
     csrcs = [str(CSRC / s) for s in COMPAT_SOURCES if (CSRC / s).exists()]
     if csrcs:
-        _run(["g++", "-O2", "-std=c++20", "-fPIC", "-shared", "-I", str(ROOT / "include"),
-              "-o", str(compat), *csrcs, f"-L{PKG}", "-lfa3b",
-              "-Wl,-rpath,$ORIGIN"])
+        _run(["g++", "-O2", "-std=c++20", "-Wall", "-fPIC", "-shared", "-I", str(ROOT / "include"),
+              "-I", f"{CUDA_HOME}/include", "-o", str(compat), *csrcs, f"-L{PKG}", "-lfa3b",
+              f"-L{CUDA_HOME}/lib64", "-lcudart", "-Wl,--no-undefined",
+              f"-Wl,-rpath,$ORIGIN:{CUDA_HOME}/lib64"])
     stamp.write_text(digest)
     return out
 
