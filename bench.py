@@ -221,8 +221,21 @@ def time_fwd(api, torch, q, k, v, causal, iters, warmup, stream):
     return sum(a.elapsed_time(b) for a, b in ev) / iters
 
 
+def _time(fn, torch, stream, iters=10, warmup=3):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(iters):
+        fn()
+    b.record(stream)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / iters
+
+
 def sweep(api, torch, dev, stream):
-    """C2 sweep (16k tokens per point, hidden 2048) plus C5 (Llama-3-70B GQA)."""
+    """C2 sweep (16k tokens per point, hidden 2048), C3 FP8, C4 backward, C5 (Llama-3-70B GQA)."""
     out = []
     pts = [(n, 128, c) for n in (512, 1024, 2048, 4096, 8192, 16384) for c in (False, True)]
     pts += [(8192, 64, False), (8192, 64, True), (8192, 256, False), (8192, 256, True)]
@@ -234,6 +247,42 @@ def sweep(api, torch, dev, stream):
                     "heads": H, "causal": causal,
                     "tflops": flops_fwd(B, H, n, d, causal) / ms / 1e9, "ms": ms})
         del q, k, v
+    # C3: FP8 forward (K6 on prepared e4m3 operands; K5 timed separately)
+    for d in (128, 256):
+        for causal in (False, True):
+            B, H, n = 2, 2048 // d, 8192
+            x = [torch.randn(B, n, H, d, device=dev, dtype=torch.bfloat16) for _ in range(3)]
+            pr = [api.fp8_prepare(t, block_rows=128, hadamard=i < 2, seed=1, stream=stream)
+                  for i, t in enumerate(x)]
+            ms = _time(lambda: api.fwd(pr[0][0], pr[1][0], pr[2][0], causal=causal,
+                                       q_scale=pr[0][1], k_scale=pr[1][1], v_scale=pr[2][1],
+                                       stream=stream), torch, stream)
+            out.append({"pass": "fwd", "dtype": "e4m3", "seqlen": n, "head_dim": d, "batch": B,
+                        "heads": H, "causal": causal,
+                        "tflops": flops_fwd(B, H, n, d, causal) / ms / 1e9, "ms": ms})
+            if not causal:
+                ms = _time(lambda: api.fp8_prepare(x[0], block_rows=128, hadamard=True, seed=1,
+                                                   stream=stream), torch, stream)
+                out.append({"pass": "fp8_prepare", "head_dim": d, "elements": x[0].numel(),
+                            "gbs": x[0].numel() * 3 / ms / 1e6, "ms": ms})
+            del x, pr
+    # C4: backward (K2-K4 through fa3b_bwd)
+    for d in (128, 64):
+        for causal in (False, True):
+            B, H, n = 2, 2048 // d, 8192
+            q, k, v, do = (torch.randn(B, n, H, d, device=dev, dtype=torch.bfloat16)
+                           for _ in range(4))
+            o, lse = api.fwd(q, k, v, causal=causal, stream=stream)
+            ws = torch.empty(api.bwd_workspace_bytes(B, H, H, n, d), dtype=torch.uint8,
+                             device=dev)
+            grads = [torch.empty_like(x) for x in (q, k, v)]
+            ms = _time(lambda: api.bwd(q, k, v, o, do, lse, causal=causal, dq=grads[0],
+                                       dk=grads[1], dv=grads[2], workspace=ws, stream=stream),
+                       torch, stream)
+            out.append({"pass": "bwd", "dtype": "bf16", "seqlen": n, "head_dim": d, "batch": B,
+                        "heads": H, "causal": causal,
+                        "tflops": 2.5 * flops_fwd(B, H, n, d, causal) / ms / 1e9, "ms": ms})
+            del q, k, v, do, o, lse, ws, grads
     q = torch.randn(1, 8192, 64, 128, device=dev, dtype=torch.bfloat16)
     k, v = (torch.randn(1, 8192, 8, 128, device=dev, dtype=torch.bfloat16) for _ in range(2))
     for causal in (False, True):
@@ -250,13 +299,19 @@ def run_ours(args, rank, world, local_rank):
     import torch.distributed as dist
     from paper_2407_08608_b200 import _lib, api
 
+    from paper_2407_08608_b200.shard import max_over_ranks, partition
+
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     lib = _lib.load()
     w = WORKLOAD
-    B, H, Hkv, N, D, causal = (w["batch"], w["heads"], w["heads_kv"], w["seqlen"],
-                               w["head_dim"], w["causal"])
-    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    H, Hkv, N, D, causal = (w["heads"], w["heads_kv"], w["seqlen"], w["head_dim"], w["causal"])
+    # weak scaling: the global batch grows with the world; each rank owns whole
+    # (batch, kv-head) units of it and never exchanges data with the others
+    shard = partition(w["batch"] * world, Hkv, world)[rank]
+    b0, b1 = shard.batch_range(Hkv)
+    B = b1 - b0
+    gen = torch.Generator(device=dev).manual_seed(1234 + b0)
     q = torch.randn(B, N, H, D, device=dev, dtype=torch.bfloat16, generator=gen)
     k = torch.randn(B, N, Hkv, D, device=dev, dtype=torch.bfloat16, generator=gen)
     v = torch.randn(B, N, Hkv, D, device=dev, dtype=torch.bfloat16, generator=gen)
@@ -292,12 +347,8 @@ def run_ours(args, rank, world, local_rank):
         t_all1.record(stream)
         torch.cuda.synchronize()
     barrier()
-    total_ms = t_all0.elapsed_time(t_all1)
+    total_ms = max_over_ranks(t_all0.elapsed_time(t_all1), device=dev)
     kernel_ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
-    t = torch.tensor([total_ms], device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
     value = step_flops * world / (ms_per_step * 1e-3) / 1e12
 
@@ -325,11 +376,7 @@ def run_ours(args, rank, world, local_rank):
             e2e_step()
         e1.record(stream)
         torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1) / e2e_steps
-    t = torch.tensor([e2e_ms], device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e_ms = float(t.item())
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / e2e_steps, device=dev)
     h2d = sum(x.numel() * x.element_size() for x in (qh, kh, vh))
     d2h = oh.numel() * oh.element_size() + lh.numel() * lh.element_size()
 
@@ -349,7 +396,8 @@ def run_ours(args, rank, world, local_rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (torch.randn bf16 Q/K/V on device)",
-        "config": {"workload": w["name"], "global_batch": B * world, "seq_len": N, "heads": H,
+        "config": {"workload": w["name"], "global_batch": w["batch"] * world, "seq_len": N,
+                   "heads": H,
                    "heads_kv": Hkv, "head_dim": D, "causal": causal,
                    "parallelism": f"batch-sharded x{world} (no collectives)",
                    "l2": "no flush; inputs larger than L2 (Q+K+V+O = "
