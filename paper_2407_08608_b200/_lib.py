@@ -148,7 +148,7 @@ def load() -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    path = Path(os.environ.get("FA3B_LIB", LIB_PATH))
+    path = Path(os.environ.get("FA3B_LIB", LIB_PATH)).resolve()
     if not path.exists():
         raise RuntimeError(
             f"fa3b CUDA library not found at {path}; run __graft_entry__.build() "

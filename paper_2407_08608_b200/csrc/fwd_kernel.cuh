@@ -8,11 +8,14 @@
 // per-tile KV block count.
 //
 // CTA layout (NT query tiles of 128 rows, KV blocks of 128 rows):
-//   warps [0, 4*NT)   softmax warpgroup t owns query tile t; thread r <-> row r
-//                     <-> TMEM lane r
-//   warp 4*NT         TMA producer: Q tiles once, then K_j, V_j through a ring
+//   warps [0, 8*NT)   two softmax warpgroups per query tile t; warp w handles
+//                     rows 32 (w % 4) + lane (= TMEM lanes) and the column half
+//                     (w / 4) % 2 of S; the halves exchange row maxima through
+//                     shared memory (one named barrier per iteration) and keep
+//                     separate row sums until the epilogue
+//   warp 8*NT         TMA producer: Q tiles once, then K_j, V_j through a ring
 //                     of STAGES shared-memory slots
-//   warp 4*NT+1       MMA issuer (one elected thread), TMEM allocator
+//   warp 8*NT+1       MMA issuer (one elected thread), TMEM allocator
 // TMEM (512 columns): S_t at [128 t, 128 t + 128), P_t (16-bit, 2 per column)
 // aliased onto the first 64 columns of S_t, O_t at [128 NT + D t, + D).
 //
@@ -45,6 +48,22 @@
 
 namespace fa3b {
 
+// Optional phase tracing (compile with -DFA3B_TRACE): CTA (0,0,0) records
+// clock64() at the softmax / MMA phase boundaries of each KV iteration into
+// g_fa3b_trace[tile][iter][point]; read back with fa3b_debug_trace().
+#ifdef FA3B_TRACE
+__device__ unsigned long long g_fa3b_trace[2][64][8];
+#define FA3B_TP(t, j, k)                                                               \
+  do {                                                                                 \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (j) < 64) \
+      g_fa3b_trace[t][j][k] = clock64();                                               \
+  } while (0)
+#else
+#define FA3B_TP(t, j, k) \
+  do {                   \
+  } while (0)
+#endif
+
 enum FwdKind { KIND_F16 = 0, KIND_BF16 = 1, KIND_E4M3 = 2 };
 
 struct FwdArgs {
@@ -75,23 +94,31 @@ struct FwdTraits {
   static constexpr int CHUNKS = D / CHUNK_ELEMS;
   static constexpr int TILE_BYTES = CHUNKS * CHUNK_BYTES;
   static constexpr int STAGES = TILE_BYTES <= 16384 ? 8 : (TILE_BYTES <= 32768 ? 4 : 2);
-  static constexpr int NUM_THREADS = NT * 128 + 64;
-  static constexpr int LOAD_WARP = NT * 4;
-  static constexpr int MMA_WARP = NT * 4 + 1;
+  // two softmax warpgroups per query tile, each owning 64 of the 128 columns
+  static constexpr int NUM_THREADS = NT * 256 + 64;
+  static constexpr int LOAD_WARP = NT * 8;
+  static constexpr int MMA_WARP = NT * 8 + 1;
   static constexpr uint32_t TMEM_COLS = 512;
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_KV = NT * TILE_BYTES;
   static constexpr int OFF_BAR = OFF_KV + STAGES * TILE_BYTES;
   // q_full, kv_full[S], kv_empty[S], s_full[NT], p_full[NT], o_full[NT]
   static constexpr int NUM_BARS = 1 + 2 * STAGES + 3 * NT;
-  static constexpr int SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16 + 1024;
+  // row-max / row-sum exchange between the two column halves: [NT][2 buf][2 half][128]
+  static constexpr int OFF_XCH = OFF_BAR + NUM_BARS * 8 + 16;
+  static constexpr int SMEM_BYTES = OFF_XCH + NT * 2 * 2 * 128 * 4 + 1024;
   static_assert(NT * (128 + D) <= 512, "TMEM budget");
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
   __host__ __device__ static constexpr int s_col(int t) { return t * 128; }
   __host__ __device__ static constexpr int o_col(int t) { return NT * 128 + t * D; }
 };
 
-template <int D, int NT, bool CAUSAL, int KIND>
+// EMU: how many of every 8 exp2 pairs run on the FMA-pipe polynomial.
+#ifndef FA3B_FWD_EMU
+#define FA3B_FWD_EMU 2
+#endif
+
+template <int D, int NT, bool CAUSAL, int KIND, int EMU = FA3B_FWD_EMU>
 __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2>::NUM_THREADS, 1)
     fa3b_fwd_kernel(const __grid_constant__ CUtensorMap tmQ,
                     const __grid_constant__ CUtensorMap tmK,
@@ -139,7 +166,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2>::N
       }
       for (int t = 0; t < NT; ++t) {
         ptx::mbar_init(&s_full[t], 1);
-        ptx::mbar_init(&p_full[t], 128);
+        ptx::mbar_init(&p_full[t], 8);  // one arrival per softmax warp
         ptx::mbar_init(&o_full[t], 1);
       }
       ptx::fence_mbar_init();
@@ -243,6 +270,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2>::N
         for (int t = 0; t < NT; ++t) {
           if (j >= n_t[t]) continue;
           ptx::mbar_wait(&p_full[t], j & 1);
+          FA3B_TP(t, j, 6);
           ptx::tc_fence_after();
           issue_pv(t, slot_v, j > 0);
           if (j + 1 < n_t[t]) {
@@ -263,13 +291,18 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2>::N
     }
   } else {
     // ------------------------------------------------------------ softmax
-    const int t = warp >> 2;
-    const int r = threadIdx.x & 127;
+    const int t = warp >> 3;             // query tile
+    const int hh = (warp >> 2) & 1;      // column half of S / O
+    const int r = ((warp & 3) << 5) | static_cast<int>(ptx::lane_id());  // row == TMEM lane
     const uint32_t lane_base = static_cast<uint32_t>(32 * (warp & 3)) << 16;
     const uint32_t tS = tmem + lane_base + T::s_col(t);
     const uint32_t tO = tmem + lane_base + T::o_col(t);
+    float* xch = reinterpret_cast<float*>(smem + T::OFF_XCH) + t * 512;  // [2 buf][2 half][128]
+    const uint32_t bar_id = 1 + t;
     const int q_row = q_base + t * 128 + r;
     const int nt = (t == 0) ? n_t[0] : n_t[NT - 1];
+    constexpr int HC = 64;               // columns per half
+    constexpr int DH = D / 2;            // O columns per half
     float sl2 = args.scale_log2;
     float thr = 8.f;
     float out_scale = 1.f;
@@ -285,8 +318,8 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2>::N
       thr = args.fp8_thr;
     }
     float v_cur = 0.f;  // V scale the O accumulator is expressed in (FP8)
-    float m_use = -INFINITY;  // running max in use, scaled log2 units
-    float l = 0.f;
+    float m_use = -INFINITY;  // running max in use, scaled log2 units (same in both halves)
+    float l = 0.f;            // this half's share of the row sum
     for (int j = 0; j < nt; ++j) {
       float slj = sl2;
       float pmul = 1.f;
@@ -300,86 +333,122 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2>::N
         }
         pmul = 448.f * ptx::ex2(-thr);  // e4m3 codes of P: P * 448 / 2^thr
       }
+      const bool tr = (warp & 7) == 0 && ptx::lane_id() == 0;
+      if (tr) FA3B_TP(t, j, 0);
       ptx::mbar_wait(&s_full[t], j & 1);
+      if (tr) FA3B_TP(t, j, 1);
       ptx::tc_fence_after();
-      uint32_t sr[128];
+      float s[HC];
+      const int kv0 = j * 128 + HC * hh;
+      const bool need_mask = (j * 128 + 128 > N) || (CAUSAL && j == nt - 1);
+      auto load_s = [&]() {
+        uint32_t sr[HC];
+        ptx::tmem_ld32(tS + HC * hh, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+        ptx::tmem_ld32(tS + HC * hh + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+        ptx::tmem_wait_ld();
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
-        ptx::tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
-      ptx::tmem_wait_ld();
-      float s[128];
+        for (int i = 0; i < HC; ++i) s[i] = __uint_as_float(sr[i]);
+        if (need_mask) {
+          const int lim = (CAUSAL ? min(q_row + 1, N) : N) - kv0;
 #pragma unroll
-      for (int i = 0; i < 128; ++i) s[i] = __uint_as_float(sr[i]);
-      const int kv0 = j * 128;
-      const bool need_mask = (kv0 + 128 > N) || (CAUSAL && j == nt - 1);
-      if (need_mask) {
-        const int lim = (CAUSAL ? min(q_row + 1, N) : N) - kv0;
+          for (int i = 0; i < HC; ++i) s[i] = (i < lim) ? s[i] : -INFINITY;
+        }
+      };
+      load_s();
+      if (tr) FA3B_TP(t, j, 2);
+      // half-row max: FMNMX3 over 4 independent chains, then swap with the other half
+      float a0 = s[0], a1 = s[1], a2 = s[2], a3 = s[3];
 #pragma unroll
-        for (int i = 0; i < 128; ++i) s[i] = (i < lim) ? s[i] : -INFINITY;
+      for (int i = 4; i < 60; i += 8) {
+        a0 = ptx::max3(a0, s[i], s[i + 1]);
+        a1 = ptx::max3(a1, s[i + 2], s[i + 3]);
+        a2 = ptx::max3(a2, s[i + 4], s[i + 5]);
+        a3 = ptx::max3(a3, s[i + 6], s[i + 7]);
       }
-      float mx = s[0];
+      a0 = ptx::max3(a0, s[60], s[61]);
+      a1 = ptx::max3(a1, s[62], s[63]);
+      const float pm = fmaxf(ptx::max3(a0, a1, a2), a3);
+      float* xb = xch + (j & 1) * 256;
+      xb[hh * 128 + r] = pm;
+      // P = 2^(s * slj - msub) for this half: FFMA2 pairs; EMU of every 8 pairs go
+      // through the FMA-pipe polynomial, the rest through MUFU.EX2; FADD2 sums.
+      constexpr int NPK = FP8 ? 16 : 32;
+      uint32_t pk[NPK];
+      float psum = 0.f;
+      auto exp_half = [&](float msub) {
+        const float2 sc2 = make_float2(slj, slj), nm2 = make_float2(-msub, -msub);
+        float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                         make_float2(0.f, 0.f)};
+        float2 prev = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int i = 1; i < 128; ++i) mx = fmaxf(mx, s[i]);
+        for (int i = 0; i < HC / 2; ++i) {
+          const float2 x = __ffma2_rn(make_float2(s[2 * i], s[2 * i + 1]), sc2, nm2);
+          float2 pp;
+          if ((i & 7) < EMU) {
+            pp = ptx::ex2_poly2(x);
+          } else {
+            pp.x = ptx::ex2(x.x);
+            pp.y = ptx::ex2(x.y);
+          }
+          acc[i & 3] = __fadd2_rn(acc[i & 3], pp);
+          if constexpr (FP8) {
+            if (i & 1)
+              pk[i >> 1] = ptx::pack_e4m3x4(prev.x * pmul, prev.y * pmul, pp.x * pmul, pp.y * pmul);
+            else
+              prev = pp;
+          } else {
+            pk[i] = BF16 ? ptx::pack_bf16(pp.x, pp.y) : ptx::pack_f16(pp.x, pp.y);
+          }
+        }
+        const float2 a4 = __fadd2_rn(__fadd2_rn(acc[0], acc[1]), __fadd2_rn(acc[2], acc[3]));
+        psum = a4.x + a4.y;
+      };
+      ptx::named_bar_sync(bar_id, 256);  // also: every S load of this tile has completed
+      const float mx = fmaxf(pm, xb[(hh ^ 1) * 128 + r]);
+      if (tr) FA3B_TP(t, j, 3);
       const float m_new = fmaxf(m_use, mx * slj);
       const bool resc = m_new > m_use + thr;
       const float m_cur = resc ? m_new : m_use;
       const float factor = resc ? ptx::ex2(m_use - m_new) : 1.f;
-      const float msub = (m_cur == -INFINITY) ? 0.f : m_cur;
-      float sum0 = 0.f, sum1 = 0.f;
-      if constexpr (FP8) {
-        uint32_t pk[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float p0 = ptx::ex2(fmaf(s[4 * i], slj, -msub));
-          const float p1 = ptx::ex2(fmaf(s[4 * i + 1], slj, -msub));
-          const float p2 = ptx::ex2(fmaf(s[4 * i + 2], slj, -msub));
-          const float p3 = ptx::ex2(fmaf(s[4 * i + 3], slj, -msub));
-          sum0 += p0 + p2;
-          sum1 += p1 + p3;
-          pk[i] = ptx::pack_e4m3x4(p0 * pmul, p1 * pmul, p2 * pmul, p3 * pmul);
-        }
-        ptx::tmem_st32(tS, pk);
-      } else {
-        uint32_t pk[64];
-#pragma unroll
-        for (int i = 0; i < 64; ++i) {
-          const float p0 = ptx::ex2(fmaf(s[2 * i], slj, -msub));
-          const float p1 = ptx::ex2(fmaf(s[2 * i + 1], slj, -msub));
-          sum0 += p0;
-          sum1 += p1;
-          pk[i] = BF16 ? ptx::pack_bf16(p0, p1) : ptx::pack_f16(p0, p1);
-        }
-        ptx::tmem_st32(tS, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
-        ptx::tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
-      }
-      l = l * factor + (sum0 + sum1);
+      exp_half((m_cur == -INFINITY) ? 0.f : m_cur);
+      if constexpr (FP8)
+        ptx::tmem_st16(tS + 16 * hh, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
+      else
+        ptx::tmem_st32(tS + 32 * hh, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+      l = l * factor + psum;
+      if (tr) FA3B_TP(t, j, 4);
       const float ofac = factor * vfac;
       if (j > 0 && __any_sync(0xffffffffu, ofac != 1.f)) {
-        // PV(V_{j-1}) is complete (see header); rescale this row of O_t,
-        // up to 128 columns per batch of TMEM loads.
-        constexpr int G = D / 32 < 4 ? D / 32 : 4;
+        // PV(V_{j-1}) is complete (see header); rescale this half-row of O_t.
+        constexpr int G = DH / 32 < 4 ? DH / 32 : 4;
 #pragma unroll
-        for (int c0 = 0; c0 < D / 32; c0 += G) {
+        for (int c0 = 0; c0 < DH / 32; c0 += G) {
           uint32_t ov[G][32];
 #pragma unroll
-          for (int c = 0; c < G; ++c) ptx::tmem_ld32(tO + (c0 + c) * 32, ov[c]);
+          for (int c = 0; c < G; ++c) ptx::tmem_ld32(tO + DH * hh + (c0 + c) * 32, ov[c]);
           ptx::tmem_wait_ld();
 #pragma unroll
           for (int c = 0; c < G; ++c) {
 #pragma unroll
             for (int i = 0; i < 32; ++i)
               ov[c][i] = __float_as_uint(__uint_as_float(ov[c][i]) * ofac);
-            ptx::tmem_st32(tO + (c0 + c) * 32, ov[c]);
+            ptx::tmem_st32(tO + DH * hh + (c0 + c) * 32, ov[c]);
           }
         }
       }
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
-      ptx::mbar_arrive(&p_full[t]);
+      __syncwarp();
+      if (tr) FA3B_TP(t, j, 5);
+      if (ptx::lane_id() == 0) ptx::mbar_arrive(&p_full[t]);  // one arrival per warp
       m_use = m_cur;
     }
     if (nt > 0) {
       // ---------------------------------------------------------- epilogue
+      float* xb = xch + (nt & 1) * 256;
+      xb[hh * 128 + r] = l;
+      ptx::named_bar_sync(bar_id, 256);
+      l += xb[(hh ^ 1) * 128 + r];
       ptx::mbar_wait(&o_full[t], 0);
       ptx::tc_fence_after();
       if constexpr (FP8) out_scale = v_cur * ptx::ex2(thr) * (1.f / 448.f);
@@ -387,11 +456,11 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2>::N
       const bool row_ok = q_row < N;
       const size_t obase = static_cast<size_t>(b) * args.o_sb +
                            static_cast<size_t>(q_row) * args.o_ss +
-                           static_cast<size_t>(h) * args.o_sh;
+                           static_cast<size_t>(h) * args.o_sh + DH * hh;
 #pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
+      for (int c = 0; c < DH / 32; ++c) {
         uint32_t ov[32];
-        ptx::tmem_ld32(tO + c * 32, ov);
+        ptx::tmem_ld32(tO + DH * hh + c * 32, ov);
         ptx::tmem_wait_ld();
         if (!row_ok) continue;
         if (args.out_f32) {
@@ -416,7 +485,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2>::N
             dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
         }
       }
-      if (row_ok && args.lse != nullptr) {
+      if (hh == 0 && row_ok && args.lse != nullptr) {
         const float lse = l > 0.f ? (m_use + log2f(l)) * 0.69314718055994531f : -INFINITY;
         args.lse[(static_cast<size_t>(b) * args.H + h) * N + q_row] = lse;
       }
