@@ -8,6 +8,7 @@
 //   test_flashlab_compat                     everything (needs the B200)
 #include <cmath>
 #include <cstdio>
+#include <cstdint>
 #include <cstring>
 #include <random>
 #include <stdexcept>
@@ -46,6 +47,20 @@ static fl::Matrix gaussian(std::size_t r, std::size_t c, unsigned seed) {
   std::normal_distribution<double> n(0.0, 1.0);
   fl::Matrix m(r, c);
   for (std::size_t i = 0; i < m.size(); ++i) m.data()[i] = n(g);
+  return m;
+}
+
+// RNE to bf16 (the default device format), so the FP64 oracle sees exactly the
+// values the kernels see (the reference's tests round with round_to the same way)
+static fl::Matrix bf16_rounded(fl::Matrix m) {
+  for (std::size_t i = 0; i < m.size(); ++i) {
+    float f = static_cast<float>(m.data()[i]);
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    u = (u + 0x7FFFu + ((u >> 16) & 1u)) & 0xFFFF0000u;
+    std::memcpy(&f, &u, 4);
+    m.data()[i] = f;
+  }
   return m;
 }
 
@@ -130,7 +145,8 @@ static void validation_tests() {
 static void device_tests() {
   // forward, three schedules, causal + ragged (test_flash_fwd.cpp:106-118)
   for (bool causal : {false, true}) {
-    auto in = fl::attention_inputs(gaussian(300, 64, 10), gaussian(300, 64, 11), gaussian(300, 64, 12), causal);
+    auto in = fl::attention_inputs(bf16_rounded(gaussian(300, 64, 10)), bf16_rounded(gaussian(300, 64, 11)),
+                                   bf16_rounded(gaussian(300, 64, 12)), causal);
     const Dense ref = dense_fwd(in);
     for (int sched = 0; sched < 3; ++sched) {
       const fl::ForwardOutput out = sched == 0   ? fl::flash_fwd_basic(in, {64, 64})
@@ -140,6 +156,7 @@ static void device_tests() {
       double lerr = 0;
       for (std::size_t i = 0; i < 300; ++i) lerr = std::max(lerr, std::fabs(out.logsumexp[i] - ref.lse[i]));
       CHECK(lerr < 1e-3);
+      if (lerr >= 1e-3) std::fprintf(stderr, "  causal=%d sched=%d max|dLSE|=%g\n", causal, sched, lerr);
     }
   }
   // structural probes (test_flash_fwd.cpp:139-150)
