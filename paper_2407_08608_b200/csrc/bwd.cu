@@ -97,12 +97,6 @@ __global__ void fa3b_bwd_dq_kernel(const float* __restrict__ dq_acc, int Npad, i
                             h * q_sh + c8 * 8) = out;
 }
 
-__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b),
-               "f"(c), "f"(d)
-               : "memory");
-}
-
 struct BwdArgs {
   int B, H, Hkv, N, Npad, group;
   float scale_log2;  // |alpha| log2e
@@ -116,26 +110,48 @@ struct BwdArgs {
   long long dv_sb, dv_ss, dv_sh;
 };
 
+// K3 layout. Warps 0-7: two gradient warpgroups (warpgroup w owns query columns
+// [64 w, 64 w + 64) of the S^T / dP^T tile; thread r owns KV row r = TMEM lane r);
+// warps 8-11: the dQ-writer warpgroup; warp 12: TMA producer; warp 13: MMA issuer.
+//
+// TMEM (512 columns): S^T [0,128) (P^T as 16-bit pairs over its first 32 columns of
+// each warpgroup half), dP^T [128,256) (dS^T pairs likewise), dV [256, 256+D),
+// dK [256+D, 256+2D). dQ: for D = 128 the transposed product dQ_i^T = K^T dS_i^T
+// reuses the dP^T columns (TMEM lane = head-dim index, so the dQ-writer's
+// red.global.add.f32 from one warp covers 32 consecutive floats of one query row:
+// one 128-byte line per instruction); for D = 64 (M = 64 would be a half-rate
+// MMA) dQ_i = dS_i K goes to its own columns [384, 448) and leaves through a
+// swizzled shared-memory box and a TMA reduce-add (cp.reduce.async.bulk.tensor).
+//
+// Per Q tile i the MMA order is
+//   dV += P_i^T dO_i | dK += dS_i^T Q_i | S_{i+1} = K Q_{i+1}^T | dQ_i | dP_{i+1} = V dO_{i+1}^T
+// with the softmax split in two phases (P_i after S_i lands, dS_i after dP_i), so
+// dV_i starts while dS_i is still being formed and S_{i+1} runs under the dQ drain.
 template <int D_>
 struct BwdTraits {
   static constexpr int D = D_;
   static constexpr int CHUNK_BYTES = 128 * 128;
   static constexpr int TILE_BYTES = (D / 64) * CHUNK_BYTES;  // 128 rows x D 16-bit
-  static constexpr int NUM_THREADS = 256 + 64;
-  static constexpr int LOAD_WARP = 8;
-  static constexpr int MMA_WARP = 9;
+  static constexpr bool DQ_T = (D == 128);
+  static constexpr int DRAIN_WARP0 = 8;
+  static constexpr int LOAD_WARP = 12;
+  static constexpr int MMA_WARP = 13;
+  static constexpr int NUM_THREADS = 14 * 32;
   static constexpr int OFF_K = 0;
   static constexpr int OFF_V = TILE_BYTES;
-  static constexpr int OFF_Q = 2 * TILE_BYTES;          // 2 stages
-  static constexpr int OFF_DO = 4 * TILE_BYTES;         // 2 stages
-  static constexpr int OFF_DS = 6 * TILE_BYTES;         // 128 x 128 16-bit, MN-major
-  static constexpr int OFF_BAR = OFF_DS + 2 * CHUNK_BYTES;
-  // kv_full, q_full[2], q_empty[2], s_full, p_full, dq_full, dq_empty, dkv_full
-  static constexpr int NUM_BARS = 10;
-  static constexpr int SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16 + 1024;
+  static constexpr int OFF_Q = 2 * TILE_BYTES;   // 2 stages
+  static constexpr int OFF_DO = 4 * TILE_BYTES;  // 2 stages
+  static constexpr int OFF_DS = 6 * TILE_BYTES;  // 128 kv x 128 q 16-bit, K-major per 64-q chunk
+  static constexpr int OFF_STG = OFF_DS + 2 * CHUNK_BYTES;  // D = 64: dQ box 2 x (128 x 32 fp32)
+  static constexpr int STG_BYTES = DQ_T ? 0 : 2 * CHUNK_BYTES;
+  static constexpr int OFF_VEC = OFF_STG + STG_BYTES;  // LSE2[2][128], Delta[2][128] fp32
+  static constexpr int OFF_BAR = OFF_VEC + 4 * 512;
+  // kv_full, q_full[2], q_empty[2], s_full, dp_full, pa_full, pb_full, dq_full, dq_free, dkv_full
+  static constexpr int NUM_BARS = 12;
+  static constexpr int SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr int COL_S = 0, COL_DP = 128, COL_DV = 256, COL_DK = 256 + D;
-  static constexpr bool ALIAS_DQ = (COL_DK + D + D > 512);
-  static constexpr int COL_DQ = ALIAS_DQ ? 0 : COL_DK + D;
+  static constexpr int COL_DQ = DQ_T ? COL_DP : 256 + 2 * D;
+  static constexpr int EMU = D == 64 ? 2 : 0;  // exp2 pairs (of 8) on the FMA-pipe polynomial
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 };
 
@@ -147,34 +163,39 @@ template <int D, bool CAUSAL, bool BF16>
 __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
     fa3b_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-                    const BwdArgs args, const uint32_t idesc_s, const uint32_t idesc_dp,
-                    const uint32_t idesc_acc, const uint32_t idesc_dq) {
+                    const __grid_constant__ CUtensorMap tmDQ, const BwdArgs args,
+                    const uint32_t idesc_s, const uint32_t idesc_dp, const uint32_t idesc_acc,
+                    const uint32_t idesc_dq) {
   using T = BwdTraits<D>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + T::OFF_BAR);
   uint64_t* kv_full = bars;
   uint64_t* q_full = bars + 1;
   uint64_t* q_empty = bars + 3;
   uint64_t* s_full = bars + 5;
-  uint64_t* p_full = bars + 6;
-  uint64_t* dq_full = bars + 7;
-  uint64_t* dq_empty = bars + 8;
-  uint64_t* dkv_full = bars + 9;
+  uint64_t* dp_full = bars + 6;
+  uint64_t* pa_full = bars + 7;
+  uint64_t* pb_full = bars + 8;
+  uint64_t* dq_full = bars + 9;
+  uint64_t* dq_free = bars + 10;
+  uint64_t* dkv_full = bars + 11;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + T::NUM_BARS);
+  float* lse_s = reinterpret_cast<float*>(smem + T::OFF_VEC);  // [2][128]
+  float* del_s = lse_s + 256;                                   // [2][128]
 
   const int warp = static_cast<int>(ptx::warp_id());
   const int j = blockIdx.x;  // KV tile
   const int hkv = blockIdx.y;
   const int b = blockIdx.z;
   const int N = args.N;
-  const int nq = (N + 127) / 128;
+  const int nq = args.Npad / 128;
   const int i0 = CAUSAL ? j : 0;
   const int per_head = nq - i0;
   const int n_iter = per_head * args.group;
 
   if (warp == T::MMA_WARP) {
+    // the tile offsets above assume a 1024-byte aligned dynamic smem base
+    if ((ptx::smem_u32(smem) & 1023u) != 0) __trap();
     if (ptx::lane_id() == 0) {
       ptx::mbar_init(kv_full, 1);
       for (int s = 0; s < 2; ++s) {
@@ -182,9 +203,11 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
         ptx::mbar_init(&q_empty[s], 1);
       }
       ptx::mbar_init(s_full, 1);
-      ptx::mbar_init(p_full, 256);
+      ptx::mbar_init(dp_full, 1);
+      ptx::mbar_init(pa_full, 8);  // one arrival per gradient warp
+      ptx::mbar_init(pb_full, 8);
       ptx::mbar_init(dq_full, 1);
-      ptx::mbar_init(dq_empty, 256);
+      ptx::mbar_init(dq_free, 4);  // one arrival per dQ-writer warp
       ptx::mbar_init(dkv_full, 1);
       ptx::fence_mbar_init();
     }
@@ -197,6 +220,7 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == T::LOAD_WARP) {
+    // ------------------------------------------------ TMA producer
     if (ptx::elect_one()) {
       ptx::prefetch_tmap(&tmQ);
       ptx::prefetch_tmap(&tmK);
@@ -204,161 +228,266 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
       ptx::prefetch_tmap(&tmdO);
       ptx::mbar_arrive_expect_tx(kv_full, 2 * T::TILE_BYTES);
       for (int c = 0; c < D / 64; ++c) {
-        ptx::tma_load_4d(smem + T::OFF_K + c * T::CHUNK_BYTES, &tmK, kv_full, c * 64, hkv, j * 128,
-                         b, ptx::kEvictNormal);
-        ptx::tma_load_4d(smem + T::OFF_V + c * T::CHUNK_BYTES, &tmV, kv_full, c * 64, hkv, j * 128,
-                         b, ptx::kEvictNormal);
+        ptx::tma_load_4d(smem + T::OFF_K + c * T::CHUNK_BYTES, &tmK, kv_full, c * 64, hkv, j * 128, b,
+                         ptx::kEvictFirst);
+        ptx::tma_load_4d(smem + T::OFF_V + c * T::CHUNK_BYTES, &tmV, kv_full, c * 64, hkv, j * 128, b,
+                         ptx::kEvictFirst);
       }
       for (int it = 0; it < n_iter; ++it) {
         const int s = it & 1;
         const int h = hkv * args.group + it / per_head;
         const int i = i0 + it % per_head;
+        const size_t vec = (static_cast<size_t>(b) * args.H + h) * args.Npad + i * 128;
         ptx::mbar_wait(&q_empty[s], ((it >> 1) & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(&q_full[s], 2 * T::TILE_BYTES);
+        ptx::mbar_arrive_expect_tx(&q_full[s], 2 * T::TILE_BYTES + 1024);
         for (int c = 0; c < D / 64; ++c) {
-          ptx::tma_load_4d(smem + T::OFF_Q + s * T::TILE_BYTES + c * T::CHUNK_BYTES, &tmQ,
-                           &q_full[s], c * 64, h, i * 128, b, ptx::kEvictLast);
-          ptx::tma_load_4d(smem + T::OFF_DO + s * T::TILE_BYTES + c * T::CHUNK_BYTES, &tmdO,
-                           &q_full[s], c * 64, h, i * 128, b, ptx::kEvictLast);
+          ptx::tma_load_4d(smem + T::OFF_Q + s * T::TILE_BYTES + c * T::CHUNK_BYTES, &tmQ, &q_full[s],
+                           c * 64, h, i * 128, b, ptx::kEvictLast);
+          ptx::tma_load_4d(smem + T::OFF_DO + s * T::TILE_BYTES + c * T::CHUNK_BYTES, &tmdO, &q_full[s],
+                           c * 64, h, i * 128, b, ptx::kEvictLast);
         }
+        ptx::bulk_load(lse_s + s * 128, args.lse2 + vec, 512, &q_full[s]);
+        ptx::bulk_load(del_s + s * 128, args.delta + vec, 512, &q_full[s]);
       }
     }
   } else if (warp == T::MMA_WARP) {
+    // ------------------------------------------------ MMA issuer
     if (ptx::elect_one()) {
       const uint32_t k_addr = ptx::smem_u32(smem + T::OFF_K);
       const uint32_t v_addr = ptx::smem_u32(smem + T::OFF_V);
       const uint32_t ds_addr = ptx::smem_u32(smem + T::OFF_DS);
-      ptx::mbar_wait(kv_full, 0);
-      for (int it = 0; it < n_iter; ++it) {
-        const int s = it & 1;
-        const uint32_t q_addr = ptx::smem_u32(smem + T::OFF_Q + s * T::TILE_BYTES);
-        const uint32_t do_addr = ptx::smem_u32(smem + T::OFF_DO + s * T::TILE_BYTES);
-        ptx::mbar_wait(&q_full[s], (it >> 1) & 1);
-        if (T::ALIAS_DQ && it > 0) ptx::mbar_wait(dq_empty, (it - 1) & 1);
-        ptx::tc_fence_after();
+      auto q_addr = [&](int s) { return ptx::smem_u32(smem + T::OFF_Q + s * T::TILE_BYTES); };
+      auto do_addr = [&](int s) { return ptx::smem_u32(smem + T::OFF_DO + s * T::TILE_BYTES); };
+      // S^T = K Q^T and dP^T = V dO^T (both operands K-major, 128B swizzle)
+      auto issue_s = [&](int s) {
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k) {  // S^T = K Q^T, dP^T = V dO^T (K-major, SW128)
+        for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = (k >> 2) * T::CHUNK_BYTES + (k & 3) * 32;
           ptx::mma_f16_ss(tmem + T::COL_S, ptx::sw128_desc(k_addr + off, 16, 1024),
-                          ptx::sw128_desc(q_addr + off, 16, 1024), idesc_s, k > 0);
-          ptx::mma_f16_ss(tmem + T::COL_DP, ptx::sw128_desc(v_addr + off, 16, 1024),
-                          ptx::sw128_desc(do_addr + off, 16, 1024), idesc_dp, k > 0);
+                          ptx::sw128_desc(q_addr(s) + off, 16, 1024), idesc_s, k > 0);
         }
-        ptx::mma_commit(s_full);
-        ptx::mbar_wait(p_full, it & 1);
+      };
+      auto issue_dp = [&](int s) {
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k >> 2) * T::CHUNK_BYTES + (k & 3) * 32;
+          ptx::mma_f16_ss(tmem + T::COL_DP, ptx::sw128_desc(v_addr + off, 16, 1024),
+                          ptx::sw128_desc(do_addr(s) + off, 16, 1024), idesc_dp, k > 0);
+        }
+      };
+      ptx::mbar_wait(kv_full, 0);
+      ptx::mbar_wait(&q_full[0], 0);
+      ptx::tc_fence_after();
+      issue_s(0);
+      ptx::mma_commit(s_full);
+      issue_dp(0);
+      ptx::mma_commit(dp_full);
+      for (int it = 0; it < n_iter; ++it) {
+        const int s = it & 1;
+        const bool more = it + 1 < n_iter;
+        // dV += P^T dO (A = P^T pairs in TMEM, B = dO MN-major)
+        ptx::mbar_wait(pa_full, it & 1);
         ptx::tc_fence_after();
 #pragma unroll
-        for (int t = 0; t < 8; ++t) {  // dV += P^T dO, dK += dS^T Q (B MN-major)
-          const uint32_t boff = t * 16 * 128;
+        for (int t = 0; t < 8; ++t)
           ptx::mma_f16_ts(tmem + T::COL_DV, tmem + T::COL_S + pair_col(t),
-                          ptx::sw128_desc(do_addr + boff, T::CHUNK_BYTES, 1024), idesc_acc,
+                          ptx::sw128_desc(do_addr(s) + t * 16 * 128, T::CHUNK_BYTES, 1024), idesc_acc,
                           (it > 0 || t > 0));
+        // dK += dS^T Q (A = dS^T pairs in TMEM, B = Q MN-major)
+        ptx::mbar_wait(pb_full, it & 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
           ptx::mma_f16_ts(tmem + T::COL_DK, tmem + T::COL_DP + pair_col(t),
-                          ptx::sw128_desc(q_addr + boff, T::CHUNK_BYTES, 1024), idesc_acc,
+                          ptx::sw128_desc(q_addr(s) + t * 16 * 128, T::CHUNK_BYTES, 1024), idesc_acc,
                           (it > 0 || t > 0));
+        ptx::mma_commit(&q_empty[s]);  // Q_i, dO_i, LSE2_i, D_i are consumed
+        if (more) {
+          ptx::mbar_wait(&q_full[s ^ 1], ((it + 1) >> 1) & 1);
+          ptx::tc_fence_after();
+          issue_s(s ^ 1);
+          ptx::mma_commit(s_full);
         }
-        if (!T::ALIAS_DQ && it > 0) {
-          ptx::mbar_wait(dq_empty, (it - 1) & 1);
+        if (!T::DQ_T && it > 0) {
+          ptx::mbar_wait(dq_free, (it - 1) & 1);
           ptx::tc_fence_after();
         }
 #pragma unroll
-        for (int t = 0; t < 8; ++t) {  // dQ_i = dS K (A and B MN-major)
+        for (int t = 0; t < 8; ++t) {  // 16 KV rows per step; every operand MN-major
           const uint32_t off = t * 16 * 128;
-          ptx::mma_f16_ss(tmem + T::COL_DQ, ptx::sw128_desc(ds_addr + off, T::CHUNK_BYTES, 1024),
-                          ptx::sw128_desc(k_addr + off, T::CHUNK_BYTES, 1024), idesc_dq, t > 0);
+          if constexpr (T::DQ_T)  // dQ^T = K^T dS^T
+            ptx::mma_f16_ss(tmem + T::COL_DQ, ptx::sw128_desc(k_addr + off, T::CHUNK_BYTES, 1024),
+                            ptx::sw128_desc(ds_addr + off, T::CHUNK_BYTES, 1024), idesc_dq, t > 0);
+          else  // dQ = dS K
+            ptx::mma_f16_ss(tmem + T::COL_DQ, ptx::sw128_desc(ds_addr + off, T::CHUNK_BYTES, 1024),
+                            ptx::sw128_desc(k_addr + off, T::CHUNK_BYTES, 1024), idesc_dq, t > 0);
         }
         ptx::mma_commit(dq_full);
-        ptx::mma_commit(&q_empty[s]);
+        if (more) {
+          if (T::DQ_T) {  // dP_{i+1} overwrites the dQ_i^T columns once they are drained
+            ptx::mbar_wait(dq_free, it & 1);
+            ptx::tc_fence_after();
+          }
+          issue_dp(s ^ 1);
+          ptx::mma_commit(dp_full);
+        }
       }
       ptx::mma_commit(dkv_full);
     }
+  } else if (warp >= T::DRAIN_WARP0) {
+    // ------------------------------------------------ dQ writer (the paper's dQ-writer role)
+    const int dw = warp - T::DRAIN_WARP0;  // TMEM lane quarter
+    const uint32_t lane_base = static_cast<uint32_t>(32 * dw) << 16;
+    const int lane = static_cast<int>(ptx::lane_id());
+    const bool leader = dw == 0 && lane == 0;
+    for (int it = 0; it < n_iter; ++it) {
+      const int h = hkv * args.group + it / per_head;
+      const int i = i0 + it % per_head;
+      const size_t row0 = (static_cast<size_t>(b) * args.H + h) * args.Npad + i * 128;
+      ptx::mbar_wait(dq_full, it & 1);
+      ptx::tc_fence_after();
+      if constexpr (T::DQ_T) {
+        // lane = head-dim index 32 dw + lane; register (c, e) = query row 64 hf + 32 c + e;
+        // two halves of 64 rows keep the register count under the 128 cap
+        float* dst = args.dq_acc + row0 * D + 32 * dw + lane;
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          uint32_t v[2][32];
+#pragma unroll
+          for (int c = 0; c < 2; ++c) ptx::tmem_ld32(tmem + lane_base + T::COL_DQ + 64 * hf + c * 32, v[c]);
+          ptx::tmem_wait_ld();
+          if (hf == 1) {
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(dq_free);
+          }
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              ptx::red_add_f32(dst + (64 * hf + 32 * c + e) * D, __uint_as_float(v[c][e]));
+        }
+      } else {
+        uint32_t v[2][32];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) ptx::tmem_ld32(tmem + lane_base + T::COL_DQ + c * 32, v[c]);
+        ptx::tmem_wait_ld();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(dq_free);
+        // query row r = TMEM lane; two 128 x 32 fp32 boxes, 128B-swizzled like the TMA map
+        if (leader) ptx::bulk_wait_group_read<0>();
+        ptx::named_bar_sync(3, 128);
+        const int r = 32 * dw + lane;
+        uint8_t* stg = smem + T::OFF_STG + r * 128;
+#pragma unroll
+        for (int bx = 0; bx < 2; ++bx)
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            *reinterpret_cast<uint4*>(stg + bx * T::CHUNK_BYTES + ((u ^ (r & 7)) << 4)) =
+                make_uint4(v[bx][4 * u], v[bx][4 * u + 1], v[bx][4 * u + 2], v[bx][4 * u + 3]);
+        ptx::fence_proxy_async_smem();
+        ptx::named_bar_sync(3, 128);
+        if (leader) {
+          ptx::tma_reduce_add_4d(&tmDQ, smem + T::OFF_STG, 0, h, i * 128, b);
+          ptx::tma_reduce_add_4d(&tmDQ, smem + T::OFF_STG + T::CHUNK_BYTES, 32, h, i * 128, b);
+          ptx::bulk_commit_group();
+        }
+      }
+    }
+    if (!T::DQ_T && leader) ptx::bulk_wait_group<0>();
   } else {
-    // ------------------------------------------------ 2 softmax/gradient warpgroups
-    const int w = warp >> 2;          // which 64-column half
+    // ------------------------------------------------ 2 gradient warpgroups
+    const int w = warp >> 2;          // which 64-column half of the query tile
     const int r = threadIdx.x & 127;  // KV row in the tile == TMEM lane
     const uint32_t lane_base = static_cast<uint32_t>(32 * (warp & 3)) << 16;
     const int kv_row = j * 128 + r;
     const float sl2 = args.scale_log2;
     uint8_t* ds_row = smem + T::OFF_DS + w * T::CHUNK_BYTES + r * 128;
     for (int it = 0; it < n_iter; ++it) {
-      const int h = hkv * args.group + it / per_head;
+      const int s = it & 1;
       const int i = i0 + it % per_head;
-      const int q0 = i * 128 + 64 * w;
-      const size_t hb = static_cast<size_t>(b) * args.H + h;
-      const float4* lse4 = reinterpret_cast<const float4*>(args.lse2 + hb * args.Npad + q0);
-      const float4* del4 = reinterpret_cast<const float4*>(args.delta + hb * args.Npad + q0);
+      const float* lse_v = lse_s + s * 128 + 64 * w;
+      const float* del_v = del_s + s * 128 + 64 * w;
+      // phase A: P^T = exp2(S^T |alpha| log2e - LSE2) -> TMEM pairs, feeds dV
       ptx::mbar_wait(s_full, it & 1);
       ptx::tc_fence_after();
-      uint32_t sr[64], dpr[64];
+      uint32_t sr[64];
       ptx::tmem_ld32(tmem + lane_base + T::COL_S + 64 * w, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-      ptx::tmem_ld32(tmem + lane_base + T::COL_S + 64 * w + 32,
-                     *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
-      ptx::tmem_ld32(tmem + lane_base + T::COL_DP + 64 * w,
-                     *reinterpret_cast<uint32_t(*)[32]>(&dpr[0]));
-      ptx::tmem_ld32(tmem + lane_base + T::COL_DP + 64 * w + 32,
-                     *reinterpret_cast<uint32_t(*)[32]>(&dpr[32]));
+      ptx::tmem_ld32(tmem + lane_base + T::COL_S + 64 * w + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
       ptx::tmem_wait_ld();
       const bool diag = CAUSAL && i == j;
-      uint32_t pk[32], dk2[32];
+      const int lim = kv_row - (i * 128 + 64 * w);  // causal: query column c is visible iff c >= lim
+      float p[64];
+      uint32_t pk[32];
+      const float2 sc2 = make_float2(sl2, sl2);
 #pragma unroll
       for (int c4 = 0; c4 < 16; ++c4) {
-        const float4 l4 = __ldg(lse4 + c4);
-        const float4 d4 = __ldg(del4 + c4);
-        const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
-        const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
-        float p[4], ds[4];
+        const float4 l4 = *reinterpret_cast<const float4*>(lse_v + 4 * c4);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int c = c4 * 4 + e;
-          float pv = ptx::ex2(fmaf(__uint_as_float(sr[c]), sl2, -lv[e]));
-          if (diag && kv_row > q0 + c) pv = 0.f;
-          p[e] = pv;
-          ds[e] = pv * (__uint_as_float(dpr[c]) - dv[e]);
-        }
-        if (BF16) {
-          pk[2 * c4] = ptx::pack_bf16(p[0], p[1]);
-          pk[2 * c4 + 1] = ptx::pack_bf16(p[2], p[3]);
-          dk2[2 * c4] = ptx::pack_bf16(ds[0], ds[1]);
-          dk2[2 * c4 + 1] = ptx::pack_bf16(ds[2], ds[3]);
-        } else {
-          pk[2 * c4] = ptx::pack_f16(p[0], p[1]);
-          pk[2 * c4 + 1] = ptx::pack_f16(p[2], p[3]);
-          dk2[2 * c4] = ptx::pack_f16(ds[0], ds[1]);
-          dk2[2 * c4 + 1] = ptx::pack_f16(ds[2], ds[3]);
+        for (int hp = 0; hp < 2; ++hp) {
+          const int c = 4 * c4 + 2 * hp;
+          const float2 x = __ffma2_rn(make_float2(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), sc2,
+                                      hp ? make_float2(-l4.z, -l4.w) : make_float2(-l4.x, -l4.y));
+          float2 pp;
+          if (((c >> 1) & 7) < T::EMU) {
+            pp = ptx::ex2_poly2(x);
+          } else {
+            pp.x = ptx::ex2(x.x);
+            pp.y = ptx::ex2(x.y);
+          }
+          if (diag) {
+            pp.x = c < lim ? 0.f : pp.x;
+            pp.y = c + 1 < lim ? 0.f : pp.y;
+          }
+          p[c] = pp.x;
+          p[c + 1] = pp.y;
+          pk[c >> 1] = BF16 ? ptx::pack_bf16(pp.x, pp.y) : ptx::pack_f16(pp.x, pp.y);
         }
       }
       ptx::tmem_st32(tmem + lane_base + T::COL_S + 64 * w, pk);
-      ptx::tmem_st32(tmem + lane_base + T::COL_DP + 64 * w, dk2);
-      // dS (KV row r, 64 query columns) into the 128B-swizzled MN-major tile
+      ptx::tmem_wait_st();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (ptx::lane_id() == 0) ptx::mbar_arrive(pa_full);
+      // phase B: dS^T = P^T o (dP^T - D) -> TMEM pairs (feeds dK) and the swizzled
+      // shared tile (feeds dQ), in two 32-column halves
+      ptx::mbar_wait(dp_full, it & 1);
+      ptx::tc_fence_after();
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        *reinterpret_cast<uint4*>(ds_row + ((u ^ (r & 7)) << 4)) =
-            make_uint4(dk2[4 * u], dk2[4 * u + 1], dk2[4 * u + 2], dk2[4 * u + 3]);
+      for (int hf = 0; hf < 2; ++hf) {
+        uint32_t dpr[32];
+        ptx::tmem_ld32(tmem + lane_base + T::COL_DP + 64 * w + 32 * hf, dpr);
+        ptx::tmem_wait_ld();
+        uint32_t dk2[16];
+#pragma unroll
+        for (int c4 = 0; c4 < 8; ++c4) {
+          const float4 d4 = *reinterpret_cast<const float4*>(del_v + 32 * hf + 4 * c4);
+          const int c = 32 * hf + 4 * c4;
+          const float2 a = __fmul2_rn(make_float2(p[c], p[c + 1]),
+                                      __fadd2_rn(make_float2(__uint_as_float(dpr[4 * c4]),
+                                                             __uint_as_float(dpr[4 * c4 + 1])),
+                                                 make_float2(-d4.x, -d4.y)));
+          const float2 bq = __fmul2_rn(make_float2(p[c + 2], p[c + 3]),
+                                       __fadd2_rn(make_float2(__uint_as_float(dpr[4 * c4 + 2]),
+                                                              __uint_as_float(dpr[4 * c4 + 3])),
+                                                  make_float2(-d4.z, -d4.w)));
+          dk2[2 * c4] = BF16 ? ptx::pack_bf16(a.x, a.y) : ptx::pack_f16(a.x, a.y);
+          dk2[2 * c4 + 1] = BF16 ? ptx::pack_bf16(bq.x, bq.y) : ptx::pack_f16(bq.x, bq.y);
+        }
+        ptx::tmem_st16(tmem + lane_base + T::COL_DP + 64 * w + 16 * hf, dk2);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int uu = 4 * hf + u;
+          *reinterpret_cast<uint4*>(ds_row + ((uu ^ (r & 7)) << 4)) =
+              make_uint4(dk2[4 * u], dk2[4 * u + 1], dk2[4 * u + 2], dk2[4 * u + 3]);
+        }
       }
       ptx::fence_proxy_async_smem();
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
-      ptx::mbar_arrive(p_full);
-
-      // drain dQ_i (TMEM lane = query row r of tile i) into the fp32 workspace
-      ptx::mbar_wait(dq_full, it & 1);
-      ptx::tc_fence_after();
-      float* dst = args.dq_acc + (hb * args.Npad + i * 128 + r) * D + w * (D / 2);
-      constexpr int NCH = D / 64;  // 32-column chunks per warpgroup half
-      uint32_t qv[NCH][32];
-#pragma unroll
-      for (int c = 0; c < NCH; ++c)
-        ptx::tmem_ld32(tmem + lane_base + T::COL_DQ + w * (D / 2) + c * 32, qv[c]);
-      ptx::tmem_wait_ld();
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(dq_empty);
-#pragma unroll
-      for (int c = 0; c < NCH; ++c)
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-          red_add_v4(dst + c * 32 + 4 * e, __uint_as_float(qv[c][4 * e]),
-                     __uint_as_float(qv[c][4 * e + 1]), __uint_as_float(qv[c][4 * e + 2]),
-                     __uint_as_float(qv[c][4 * e + 3]));
+      __syncwarp();
+      if (ptx::lane_id() == 0) ptx::mbar_arrive(pb_full);
     }
     // ------------------------------------------------ epilogue: dK, dV
     ptx::mbar_wait(dkv_full, 0);
@@ -435,6 +564,10 @@ int launch_bwd_main(const fa3b_bwd_params& p, const Workspace& ws, int Npad, cud
   if ((rc = make_tmap_4d(&tk, p.k, 2, D, p.heads_kv, p.seqlen, p.batch, 64, 128)) != FA3B_OK) return rc;
   if ((rc = make_tmap_4d(&tv, p.v, 2, D, p.heads_kv, p.seqlen, p.batch, 64, 128)) != FA3B_OK) return rc;
   if ((rc = make_tmap_4d(&tdo, p.dout, 2, D, p.heads_q, p.seqlen, p.batch, 64, 128)) != FA3B_OK) return rc;
+  // dQaccum [B, H, Npad, D] fp32 as a 4-D map with 128 x 32-float (128 B, swizzled) boxes
+  const fa3b_tensor4 acc{ws.dq_acc, static_cast<int64_t>(p.heads_q) * Npad * D, D, static_cast<int64_t>(Npad) * D};
+  CUtensorMap tdq;
+  if ((rc = make_tmap_4d(&tdq, acc, 4, D, p.heads_q, Npad, p.batch, 32, 128)) != FA3B_OK) return rc;
   BwdArgs a;
   a.B = p.batch;
   a.H = p.heads_q;
@@ -459,9 +592,11 @@ int launch_bwd_main(const fa3b_bwd_params& p, const Workspace& ws, int Npad, cud
   const uint32_t idesc_s = ptx::make_idesc(128, 128, fmt, fmt, false, false, p.alpha < 0);
   const uint32_t idesc_dp = ptx::make_idesc(128, 128, fmt, fmt, false, false, false);
   const uint32_t idesc_acc = ptx::make_idesc(128, D, fmt, fmt, false, true, false);
-  const uint32_t idesc_dq = ptx::make_idesc(128, D, fmt, fmt, true, true, false);
+  // dQ^T = K^T dS^T (M = D = 128) or dQ = dS K (M = 128 query rows, N = D = 64); all MN-major
+  const uint32_t idesc_dq = Tr::DQ_T ? ptx::make_idesc(128, 128, fmt, fmt, true, true, false)
+                                     : ptx::make_idesc(128, D, fmt, fmt, true, true, false);
   dim3 grid(Npad / 128, p.heads_kv, p.batch);
-  kern<<<grid, Tr::NUM_THREADS, Tr::SMEM_BYTES, st>>>(tq, tk, tv, tdo, a, idesc_s, idesc_dp, idesc_acc,
+  kern<<<grid, Tr::NUM_THREADS, Tr::SMEM_BYTES, st>>>(tq, tk, tv, tdo, tdq, a, idesc_s, idesc_dp, idesc_acc,
                                                       idesc_dq);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? FA3B_OK : cuda_fail(e);
