@@ -112,7 +112,10 @@ struct BwdArgs {
 
 // K3 layout. Warps 0-7: two gradient warpgroups (warpgroup w owns query columns
 // [64 w, 64 w + 64) of the S^T / dP^T tile; thread r owns KV row r = TMEM lane r);
-// warps 8-11: the dQ-writer warpgroup; warp 12: TMA producer; warp 13: MMA issuer.
+// warps 8-11: the dQ-writer warpgroup; warp 12: TMA producer; warp 13: MMA issuer;
+// warps 14-15 only complete warpgroup 3, which gives registers to the dQ writer
+// (setmaxnreg 128 -> 96 / 128 -> 160) so it can release each dQ tile's TMEM
+// columns right after one load of all 128 of them.
 //
 // TMEM (512 columns): S^T [0,128) (P^T as 16-bit pairs over its first 32 columns of
 // each warpgroup half), dP^T [128,256) (dS^T pairs likewise), dV [256, 256+D),
@@ -136,7 +139,7 @@ struct BwdTraits {
   static constexpr int DRAIN_WARP0 = 8;
   static constexpr int LOAD_WARP = 12;
   static constexpr int MMA_WARP = 13;
-  static constexpr int NUM_THREADS = 14 * 32;
+  static constexpr int NUM_THREADS = 16 * 32;
   static constexpr int OFF_K = 0;
   static constexpr int OFF_V = TILE_BYTES;
   static constexpr int OFF_Q = 2 * TILE_BYTES;   // 2 stages
@@ -151,7 +154,11 @@ struct BwdTraits {
   static constexpr int SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr int COL_S = 0, COL_DP = 128, COL_DV = 256, COL_DK = 256 + D;
   static constexpr int COL_DQ = DQ_T ? COL_DP : 256 + 2 * D;
-  static constexpr int EMU = D == 64 ? 2 : 0;  // exp2 pairs (of 8) on the FMA-pipe polynomial
+#ifndef FA3B_BWD_EMU128
+#define FA3B_BWD_EMU128 0
+#endif
+  // exp2 pairs (of every 8) evaluated on the FMA-pipe polynomial instead of MUFU.EX2
+  static constexpr int EMU = D == 64 ? 2 : FA3B_BWD_EMU128;
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 };
 
@@ -218,7 +225,9 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-
+  // each setmaxnreg dominates the code of its warpgroup's roles
+  if (warp >= 12) {
+  if constexpr (T::DQ_T) ptx::setmaxnreg_dec<96>();
   if (warp == T::LOAD_WARP) {
     // ------------------------------------------------ TMA producer
     if (ptx::elect_one()) {
@@ -334,7 +343,9 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
       }
       ptx::mma_commit(dkv_full);
     }
+  }
   } else if (warp >= T::DRAIN_WARP0) {
+    if constexpr (T::DQ_T) ptx::setmaxnreg_inc<160>();
     // ------------------------------------------------ dQ writer (the paper's dQ-writer role)
     const int dw = warp - T::DRAIN_WARP0;  // TMEM lane quarter
     const uint32_t lane_base = static_cast<uint32_t>(32 * dw) << 16;
@@ -347,26 +358,19 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
       ptx::mbar_wait(dq_full, it & 1);
       ptx::tc_fence_after();
       if constexpr (T::DQ_T) {
-        // lane = head-dim index 32 dw + lane; register (c, e) = query row 64 hf + 32 c + e;
-        // two halves of 64 rows keep the register count under the 128 cap
+        uint32_t v[4][32];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) ptx::tmem_ld32(tmem + lane_base + T::COL_DQ + c * 32, v[c]);
+        ptx::tmem_wait_ld();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(dq_free);
+        // lane = head-dim index 32 dw + lane; register (c, e) = query row 32 c + e
         float* dst = args.dq_acc + row0 * D + 32 * dw + lane;
 #pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
-          uint32_t v[2][32];
+        for (int c = 0; c < 4; ++c)
 #pragma unroll
-          for (int c = 0; c < 2; ++c) ptx::tmem_ld32(tmem + lane_base + T::COL_DQ + 64 * hf + c * 32, v[c]);
-          ptx::tmem_wait_ld();
-          if (hf == 1) {
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(dq_free);
-          }
-#pragma unroll
-          for (int c = 0; c < 2; ++c)
-#pragma unroll
-            for (int e = 0; e < 32; ++e)
-              ptx::red_add_f32(dst + (64 * hf + 32 * c + e) * D, __uint_as_float(v[c][e]));
-        }
+          for (int e = 0; e < 32; ++e) ptx::red_add_f32(dst + (32 * c + e) * D, __uint_as_float(v[c][e]));
       } else {
         uint32_t v[2][32];
 #pragma unroll
