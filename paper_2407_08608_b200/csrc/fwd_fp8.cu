@@ -92,3 +92,11 @@ int launch_fwd_fp8(const fa3b_fwd_params& p, cudaStream_t s) {
 }
 
 }  // namespace fa3b
+
+#ifdef FA3B_TRACE
+// Debug builds only: the e4m3 instantiations record into this translation unit's trace.
+extern "C" __attribute__((visibility("default"))) int fa3b_debug_trace_fp8(unsigned long long* out, int n) {
+  const size_t bytes = sizeof(unsigned long long) * static_cast<size_t>(n);
+  return cudaMemcpyFromSymbol(out, fa3b::g_fa3b_trace, bytes) == cudaSuccess ? 0 : -1;
+}
+#endif

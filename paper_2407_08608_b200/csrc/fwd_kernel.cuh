@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2>::N
           vfac = v_cur / vs;  // 0 on the first block: O is empty
           v_cur = vs;
         }
-        pmul = 448.f * ptx::ex2(-thr);  // e4m3 codes of P: P * 448 / 2^thr
+        pmul = 448.f * ptx::ex2(-thr);  // e4m3 codes of P: P * 448 / 2^thr (folded into exp2's bias)
       }
       const bool tr = (warp & 7) == 0 && ptx::lane_id() == 0;
       if (tr) FA3B_TP(t, j, 0);
@@ -375,8 +375,11 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2>::N
       constexpr int NPK = FP8 ? 16 : 32;
       uint32_t pk[NPK];
       float psum = 0.f;
+      // FP8: exp2(x + log2 pmul) gives the P codes' scale for free; the row sum is
+      // rescaled once per block instead of every element
+      const float lpm = FP8 ? __log2f(pmul) : 0.f;
       auto exp_half = [&](float msub) {
-        const float2 sc2 = make_float2(slj, slj), nm2 = make_float2(-msub, -msub);
+        const float2 sc2 = make_float2(slj, slj), nm2 = make_float2(lpm - msub, lpm - msub);
         float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                          make_float2(0.f, 0.f)};
         float2 prev = make_float2(0.f, 0.f);
@@ -393,7 +396,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2>::N
           acc[i & 3] = __fadd2_rn(acc[i & 3], pp);
           if constexpr (FP8) {
             if (i & 1)
-              pk[i >> 1] = ptx::pack_e4m3x4(prev.x * pmul, prev.y * pmul, pp.x * pmul, pp.y * pmul);
+              pk[i >> 1] = ptx::pack_e4m3x4(prev.x, prev.y, pp.x, pp.y);
             else
               prev = pp;
           } else {
@@ -415,7 +418,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2>::N
         ptx::tmem_st16(tS + 16 * hh, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
       else
         ptx::tmem_st32(tS + 32 * hh, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
-      l = l * factor + psum;
+      l = l * factor + (FP8 ? psum * (1.f / pmul) : psum);
       if (tr) FA3B_TP(t, j, 4);
       const float ofac = factor * vfac;
       if (j > 0 && __any_sync(0xffffffffu, ofac != 1.f)) {

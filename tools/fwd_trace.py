@@ -5,18 +5,26 @@ sys.path.insert(0, ".")
 from paper_2407_08608_b200 import api, _lib
 D = int(sys.argv[1]) if len(sys.argv) > 1 else 128
 causal = len(sys.argv) > 2 and sys.argv[2] == "1"
+fp8 = sys.argv[3] if len(sys.argv) > 3 else ""   # "", "block" or "tensor"
 N, B, H = 8192, 2, 2048 // D
 q, k, v = (torch.randn(B, N, H, D, device="cuda", dtype=torch.bfloat16) for _ in range(3))
-for _ in range(3): api.fwd(q, k, v, causal=causal)
+if fp8:
+    blk = 128 if fp8 == "block" else 0
+    pr = [api.fp8_prepare(x, block_rows=blk, hadamard=i < 2, seed=1) for i, x in enumerate((q, k, v))]
+    run = lambda: api.fwd(pr[0][0], pr[1][0], pr[2][0], causal=causal, q_scale=pr[0][1], k_scale=pr[1][1],
+                          v_scale=pr[2][1], q_block_rows=blk, kv_block_rows=blk)
+else:
+    run = lambda: api.fwd(q, k, v, causal=causal)
+for _ in range(3): run()
 torch.cuda.synchronize()
 lib = _lib.load()
 buf = (ctypes.c_ulonglong * (2 * 64 * 8))()
-assert lib.fa3b_debug_trace(buf, 2 * 64 * 8) == 0
+assert (lib.fa3b_debug_trace_fp8 if fp8 else lib.fa3b_debug_trace)(buf, 2 * 64 * 8) == 0
 t = np.frombuffer(buf, dtype=np.uint64).reshape(2, 64, 8).astype(np.int64)
 base = t[t > 0].min()
 t = np.where(t > 0, t - base, -1)
 names = ["wait_S", "S_ready", "ld_done", "max_done", "exp_done", "arrive_P", "mma_sawP", "-"]
-print(f"D={D} causal={causal}  (cycles since first event; per tile t, iteration j)")
+print(f"D={D} causal={causal} fp8={fp8 or None}  (cycles since first event; per tile t, iteration j)")
 for tile in range(2):
     for j in list(range(0, 6)) + list(range(30, 34)):
         r = t[tile, j]
