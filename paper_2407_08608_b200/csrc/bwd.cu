@@ -31,6 +31,21 @@
 
 namespace fa3b {
 
+// Optional phase tracing (-DFA3B_TRACE): CTA (0,0,0) records clock64() at the
+// K3 phase boundaries of each Q-tile iteration; read with fa3b_debug_bwd_trace().
+#ifdef FA3B_TRACE
+__device__ unsigned long long g_fa3b_bwd_trace[64][16];
+#define BWD_TP(it, k)                                                                      \
+  do {                                                                                     \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (it) < 64)               \
+      g_fa3b_bwd_trace[it][k] = clock64();                                                 \
+  } while (0)
+#else
+#define BWD_TP(it, k) \
+  do {                \
+  } while (0)
+#endif
+
 namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
@@ -191,9 +206,22 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
   float* del_s = lse_s + 256;                                   // [2][128]
 
   const int warp = static_cast<int>(ptx::warp_id());
-  const int j = blockIdx.x;  // KV tile
-  const int hkv = blockIdx.y;
-  const int b = blockIdx.z;
+#ifndef FA3B_CAUSAL_LPT
+#define FA3B_CAUSAL_LPT 1
+#endif
+  // causal: KV tile j sees nq - j query tiles; launch longest-first across all heads
+  int j, hkv, b;
+  if (CAUSAL && FA3B_CAUSAL_LPT) {
+    const int lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    const int hb = gridDim.y * gridDim.z;
+    j = lin / hb;
+    hkv = (lin % hb) % gridDim.y;
+    b = (lin % hb) / gridDim.y;
+  } else {
+    j = blockIdx.x;  // KV tile
+    hkv = blockIdx.y;
+    b = blockIdx.z;
+  }
   const int N = args.N;
   const int nq = args.Npad / 128;
   const int i0 = CAUSAL ? j : 0;
@@ -296,6 +324,7 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
         const bool more = it + 1 < n_iter;
         // dV += P^T dO (A = P^T pairs in TMEM, B = dO MN-major)
         ptx::mbar_wait(pa_full, it & 1);
+        BWD_TP(it, 0);
         ptx::tc_fence_after();
 #pragma unroll
         for (int t = 0; t < 8; ++t)
@@ -304,6 +333,7 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
                           (it > 0 || t > 0));
         // dK += dS^T Q (A = dS^T pairs in TMEM, B = Q MN-major)
         ptx::mbar_wait(pb_full, it & 1);
+        BWD_TP(it, 1);
         ptx::tc_fence_after();
 #pragma unroll
         for (int t = 0; t < 8; ++t)
@@ -337,6 +367,7 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
             ptx::mbar_wait(dq_free, it & 1);
             ptx::tc_fence_after();
           }
+          BWD_TP(it, 2);
           issue_dp(s ^ 1);
           ptx::mma_commit(dp_full);
         }
@@ -356,6 +387,7 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
       const int i = i0 + it % per_head;
       const size_t row0 = (static_cast<size_t>(b) * args.H + h) * args.Npad + i * 128;
       ptx::mbar_wait(dq_full, it & 1);
+      if (dw == 0 && lane == 0) BWD_TP(it, 12);
       ptx::tc_fence_after();
       if constexpr (T::DQ_T) {
         uint32_t v[4][32];
@@ -365,12 +397,17 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(dq_free);
+        if (dw == 0 && lane == 0) BWD_TP(it, 13);
         // lane = head-dim index 32 dw + lane; register (c, e) = query row 32 c + e
         float* dst = args.dq_acc + row0 * D + 32 * dw + lane;
+#ifndef FA3B_BWD_NO_RED  // diagnosis builds only: drop the dQ reduction
 #pragma unroll
         for (int c = 0; c < 4; ++c)
 #pragma unroll
           for (int e = 0; e < 32; ++e) ptx::red_add_f32(dst + (32 * c + e) * D, __uint_as_float(v[c][e]));
+#else
+        if (v[0][0] == 0x7fffffffu && dst == nullptr) ptx::red_add_f32(dst, 0.f);
+#endif
       } else {
         uint32_t v[2][32];
 #pragma unroll
@@ -414,7 +451,9 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
       const float* lse_v = lse_s + s * 128 + 64 * w;
       const float* del_v = del_s + s * 128 + 64 * w;
       // phase A: P^T = exp2(S^T |alpha| log2e - LSE2) -> TMEM pairs, feeds dV
+      const bool trc = (warp & 3) == 0 && ptx::lane_id() == 0;
       ptx::mbar_wait(s_full, it & 1);
+      if (trc) BWD_TP(it, 4 + 4 * w);
       ptx::tc_fence_after();
       uint32_t sr[64];
       ptx::tmem_ld32(tmem + lane_base + T::COL_S + 64 * w, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
@@ -454,15 +493,18 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
       ptx::tc_fence_before();
       __syncwarp();
       if (ptx::lane_id() == 0) ptx::mbar_arrive(pa_full);
+      if (trc) BWD_TP(it, 5 + 4 * w);
       // phase B: dS^T = P^T o (dP^T - D) -> TMEM pairs (feeds dK) and the swizzled
       // shared tile (feeds dQ), in two 32-column halves
       ptx::mbar_wait(dp_full, it & 1);
+      if (trc) BWD_TP(it, 6 + 4 * w);
       ptx::tc_fence_after();
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
         uint32_t dpr[32];
         ptx::tmem_ld32(tmem + lane_base + T::COL_DP + 64 * w + 32 * hf, dpr);
         ptx::tmem_wait_ld();
+        if (trc && w == 0) BWD_TP(it, hf ? 15 : 3);
         uint32_t dk2[16];
 #pragma unroll
         for (int c4 = 0; c4 < 8; ++c4) {
@@ -486,12 +528,14 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
           *reinterpret_cast<uint4*>(ds_row + ((uu ^ (r & 7)) << 4)) =
               make_uint4(dk2[4 * u], dk2[4 * u + 1], dk2[4 * u + 2], dk2[4 * u + 3]);
         }
+        if (trc && w == 0 && hf == 0) BWD_TP(it, 14);
       }
       ptx::fence_proxy_async_smem();
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
       __syncwarp();
       if (ptx::lane_id() == 0) ptx::mbar_arrive(pb_full);
+      if (trc) BWD_TP(it, 7 + 4 * w);
     }
     // ------------------------------------------------ epilogue: dK, dV
     ptx::mbar_wait(dkv_full, 0);
@@ -629,6 +673,13 @@ int launch_prep(const fa3b_tensor4& o, const fa3b_tensor4& dout, int dtype, int 
 using namespace fa3b;
 
 extern "C" {
+
+#ifdef FA3B_TRACE
+__attribute__((visibility("default"))) int fa3b_debug_bwd_trace(unsigned long long* out, int n) {
+  const size_t bytes = sizeof(unsigned long long) * static_cast<size_t>(n);
+  return cudaMemcpyFromSymbol(out, g_fa3b_bwd_trace, bytes) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 size_t fa3b_bwd_workspace_bytes(int32_t batch, int32_t heads_q, int32_t heads_kv, int32_t seqlen,
                                 int32_t head_dim) {

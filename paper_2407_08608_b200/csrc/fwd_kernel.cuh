@@ -53,6 +53,23 @@ namespace fa3b {
 // g_fa3b_trace[tile][iter][point]; read back with fa3b_debug_trace().
 #ifdef FA3B_TRACE
 __device__ unsigned long long g_fa3b_trace[2][64][8];
+// per-CTA [start globaltimer ns, SM id, end globaltimer ns, first-S-ready ns] for the first 4096 CTAs
+__device__ unsigned long long g_fa3b_cta[4096][4];
+__device__ __forceinline__ unsigned long long fa3b_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned fa3b_smid() {
+  unsigned s;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+  return s;
+}
+#define FA3B_CTA(k, v)                                                                    \
+  do {                                                                                    \
+    const unsigned cid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z); \
+    if (cid < 4096) g_fa3b_cta[cid][k] = (v);                                             \
+  } while (0)
 #define FA3B_TP(t, j, k)                                                               \
   do {                                                                                 \
     if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (j) < 64) \
@@ -61,6 +78,9 @@ __device__ unsigned long long g_fa3b_trace[2][64][8];
 #else
 #define FA3B_TP(t, j, k) \
   do {                   \
+  } while (0)
+#define FA3B_CTA(k, v) \
+  do {                 \
   } while (0)
 #endif
 
@@ -140,10 +160,31 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2>::N
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + T::NUM_BARS);
 
   const int warp = static_cast<int>(ptx::warp_id());
+#ifdef FA3B_TRACE
+  if (threadIdx.x == 0) {
+    FA3B_CTA(0, fa3b_gtime());
+    FA3B_CTA(1, fa3b_smid());
+  }
+#endif
   const int nqb = gridDim.x;
-  const int qb = CAUSAL ? (nqb - 1 - static_cast<int>(blockIdx.x)) : static_cast<int>(blockIdx.x);
-  const int h = blockIdx.y;
-  const int b = blockIdx.z;
+#ifndef FA3B_CAUSAL_LPT
+#define FA3B_CAUSAL_LPT 1
+#endif
+  // Non-causal: query blocks of one head are adjacent in launch order (K/V reuse in L2).
+  // Causal: launch order is longest-first across all heads (the linear block index
+  // walks the query blocks from the bottom of the mask up, every head at each step).
+  int qb, h, b;
+  if (CAUSAL && FA3B_CAUSAL_LPT) {
+    const int lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    const int hb = gridDim.y * gridDim.z;
+    qb = nqb - 1 - lin / hb;
+    h = (lin % hb) % gridDim.y;
+    b = (lin % hb) / gridDim.y;
+  } else {
+    qb = CAUSAL ? (nqb - 1 - static_cast<int>(blockIdx.x)) : static_cast<int>(blockIdx.x);
+    h = blockIdx.y;
+    b = blockIdx.z;
+  }
   const int hkv = h / args.group;
   const int N = args.N;
   const int q_base = qb * NT * 128;
@@ -320,23 +361,48 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2>::N
     float v_cur = 0.f;  // V scale the O accumulator is expressed in (FP8)
     float m_use = -INFINITY;  // running max in use, scaled log2 units (same in both halves)
     float l = 0.f;            // this half's share of the row sum
+    // FP8: e4m3 codes of P are P * 448 / 2^thr; exp2(x + log2 pmul) produces them directly
+    const float pmul = FP8 ? 448.f * ptx::ex2(-thr) : 1.f;
+    const float inv_pmul = FP8 ? 1.f / pmul : 1.f;
+    const float lpm = FP8 ? __log2f(pmul) : 0.f;
+#ifndef FA3B_FP8_PREFETCH
+#define FA3B_FP8_PREFETCH 0
+#endif
+    // per-block K / V scales of the next block are fetched one iteration ahead
+    float ks_next = 1.f, vs_next = 1.f;
+    if constexpr (FP8) {
+      if (nt > 0) {
+        ks_next = kscale[0];
+        vs_next = vscale[0];
+      }
+    }
     for (int j = 0; j < nt; ++j) {
       float slj = sl2;
-      float pmul = 1.f;
       float vfac = 1.f;  // O rescale for a new V block scale (uniform across the CTA)
       if constexpr (FP8) {
+#if FA3B_FP8_PREFETCH
+        slj = sl2 * ks_next;
+        const float vs = vs_next;
+        if (args.kv_blocked && j + 1 < nt) {
+          ks_next = kscale[j + 1];
+          vs_next = vscale[j + 1];
+        }
+#else
         slj = sl2 * kscale[args.kv_blocked ? j : 0];
         const float vs = vscale[args.kv_blocked ? j : 0];
+#endif
         if (vs != v_cur) {
           vfac = v_cur / vs;  // 0 on the first block: O is empty
           v_cur = vs;
         }
-        pmul = 448.f * ptx::ex2(-thr);  // e4m3 codes of P: P * 448 / 2^thr (folded into exp2's bias)
       }
       const bool tr = (warp & 7) == 0 && ptx::lane_id() == 0;
       if (tr) FA3B_TP(t, j, 0);
       ptx::mbar_wait(&s_full[t], j & 1);
       if (tr) FA3B_TP(t, j, 1);
+#ifdef FA3B_TRACE
+      if (j == 0 && threadIdx.x == 0) FA3B_CTA(3, fa3b_gtime());
+#endif
       ptx::tc_fence_after();
       float s[HC];
       const int kv0 = j * 128 + HC * hh;
@@ -369,15 +435,12 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2>::N
       a1 = ptx::max3(a1, s[62], s[63]);
       const float pm = fmaxf(ptx::max3(a0, a1, a2), a3);
       float* xb = xch + (j & 1) * 256;
-      xb[hh * 128 + r] = pm;
+      ptx::sts_f32(xb + hh * 128 + r, pm);
       // P = 2^(s * slj - msub) for this half: FFMA2 pairs; EMU of every 8 pairs go
       // through the FMA-pipe polynomial, the rest through MUFU.EX2; FADD2 sums.
       constexpr int NPK = FP8 ? 16 : 32;
       uint32_t pk[NPK];
       float psum = 0.f;
-      // FP8: exp2(x + log2 pmul) gives the P codes' scale for free; the row sum is
-      // rescaled once per block instead of every element
-      const float lpm = FP8 ? __log2f(pmul) : 0.f;
       auto exp_half = [&](float msub) {
         const float2 sc2 = make_float2(slj, slj), nm2 = make_float2(lpm - msub, lpm - msub);
         float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
@@ -407,7 +470,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2>::N
         psum = a4.x + a4.y;
       };
       ptx::named_bar_sync(bar_id, 256);  // also: every S load of this tile has completed
-      const float mx = fmaxf(pm, xb[(hh ^ 1) * 128 + r]);
+      const float mx = fmaxf(pm, ptx::lds_f32(xb + (hh ^ 1) * 128 + r));
       if (tr) FA3B_TP(t, j, 3);
       const float m_new = fmaxf(m_use, mx * slj);
       const bool resc = m_new > m_use + thr;
@@ -418,7 +481,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2>::N
         ptx::tmem_st16(tS + 16 * hh, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
       else
         ptx::tmem_st32(tS + 32 * hh, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
-      l = l * factor + (FP8 ? psum * (1.f / pmul) : psum);
+      l = l * factor + psum * inv_pmul;
       if (tr) FA3B_TP(t, j, 4);
       const float ofac = factor * vfac;
       if (j > 0 && __any_sync(0xffffffffu, ofac != 1.f)) {
@@ -449,9 +512,9 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2>::N
     if (nt > 0) {
       // ---------------------------------------------------------- epilogue
       float* xb = xch + (nt & 1) * 256;
-      xb[hh * 128 + r] = l;
+      ptx::sts_f32(xb + hh * 128 + r, l);
       ptx::named_bar_sync(bar_id, 256);
-      l += xb[(hh ^ 1) * 128 + r];
+      l += ptx::lds_f32(xb + (hh ^ 1) * 128 + r);
       ptx::mbar_wait(&o_full[t], 0);
       ptx::tc_fence_after();
       if constexpr (FP8) out_scale = v_cur * ptx::ex2(thr) * (1.f / 448.f);
@@ -497,6 +560,9 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2>::N
 
   ptx::tc_fence_before();
   __syncthreads();
+#ifdef FA3B_TRACE
+  if (threadIdx.x == 0) FA3B_CTA(2, fa3b_gtime());
+#endif
   if (warp == T::MMA_WARP) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<T::TMEM_COLS>(tmem);
