@@ -129,46 +129,57 @@ struct BwdArgs {
 // [64 w, 64 w + 64) of the S^T / dP^T tile; thread r owns KV row r = TMEM lane r);
 // warps 8-11: the dQ-writer warpgroup; warp 12: TMA producer; warp 13: MMA issuer;
 // warps 14-15 only complete warpgroup 3, which gives registers to the dQ writer
-// (setmaxnreg 128 -> 96 / 128 -> 160) so it can release each dQ tile's TMEM
-// columns right after one load of all 128 of them.
+// (setmaxnreg 128 -> 96 / 128 -> 160 at d = 128) so it can release each dQ tile's
+// TMEM columns right after one load of all of them.
 //
-// TMEM (512 columns): S^T [0,128) (P^T as 16-bit pairs over its first 32 columns of
+// TMEM (512 columns): S^T [0,128) (P^T as 16-bit pairs over the first 32 columns of
 // each warpgroup half), dP^T [128,256) (dS^T pairs likewise), dV [256, 256+D),
-// dK [256+D, 256+2D). dQ: for D = 128 the transposed product dQ_i^T = K^T dS_i^T
-// reuses the dP^T columns (TMEM lane = head-dim index, so the dQ-writer's
-// red.global.add.f32 from one warp covers 32 consecutive floats of one query row:
-// one 128-byte line per instruction); for D = 64 (M = 64 would be a half-rate
-// MMA) dQ_i = dS_i K goes to its own columns [384, 448) and leaves through a
-// swizzled shared-memory box and a TMA reduce-add (cp.reduce.async.bulk.tensor).
+// dK [256+D, 256+2D). dQ_i = dS_i K (M = 128 query rows = TMEM lanes, N = D) goes
+// to the dP^T columns at d = 128 (TMEM is full) and to its own columns [384, 448)
+// at d = 64. The dQ writer loads it, frees the columns, and sends it to the fp32
+// workspace through two 128B-swizzled 128 x 32 fp32 shared-memory boxes and TMA
+// reduce-adds (cp.reduce.async.bulk.tensor ... .add), the paper's dQ-writer role
+// without per-element atomics on the load/store pipe.
+//
+// Q_i and dO_i share a ring of tile slots (tile 2i = Q_i, 2i+1 = dO_i; 3 slots at
+// d = 128, 4 at d = 64):
+// dO_i is released after dV_i, Q_i after dK_i, which leaves room at d = 128 for
+// the dQ staging boxes. LSE2_i and D_i arrive by cp.async.bulk into their own
+// double buffer.
 //
 // Per Q tile i the MMA order is
 //   dV += P_i^T dO_i | dK += dS_i^T Q_i | S_{i+1} = K Q_{i+1}^T | dQ_i | dP_{i+1} = V dO_{i+1}^T
 // with the softmax split in two phases (P_i after S_i lands, dS_i after dP_i), so
-// dV_i starts while dS_i is still being formed and S_{i+1} runs under the dQ drain.
+// dV_i starts while dS_i is still being formed and S_{i+1} runs under dQ_i.
 template <int D_>
 struct BwdTraits {
   static constexpr int D = D_;
   static constexpr int CHUNK_BYTES = 128 * 128;
   static constexpr int TILE_BYTES = (D / 64) * CHUNK_BYTES;  // 128 rows x D 16-bit
-  static constexpr bool DQ_T = (D == 128);
+  static constexpr bool DQ_IN_DP = (D == 128);
+  // d = 128 fits three tile slots next to the dQ staging boxes; d = 64 keeps four
+  // (Q and dO each double-buffered: its GEMMs are short, so load latency shows)
+  static constexpr int RING = D == 64 ? 4 : 3;
+  // with 3 slots the LSE2/D double buffer needs its own release (Q_{i+2} reuses
+  // dO_i's slot, freed before phase B of tile i is done); with 4 it rides on Q's
+  static constexpr bool VEC_OWN = RING == 3;
   static constexpr int DRAIN_WARP0 = 8;
   static constexpr int LOAD_WARP = 12;
   static constexpr int MMA_WARP = 13;
   static constexpr int NUM_THREADS = 16 * 32;
   static constexpr int OFF_K = 0;
   static constexpr int OFF_V = TILE_BYTES;
-  static constexpr int OFF_Q = 2 * TILE_BYTES;   // 2 stages
-  static constexpr int OFF_DO = 4 * TILE_BYTES;  // 2 stages
-  static constexpr int OFF_DS = 6 * TILE_BYTES;  // 128 kv x 128 q 16-bit, K-major per 64-q chunk
-  static constexpr int OFF_STG = OFF_DS + 2 * CHUNK_BYTES;  // D = 64: dQ box 2 x (128 x 32 fp32)
-  static constexpr int STG_BYTES = DQ_T ? 0 : 2 * CHUNK_BYTES;
-  static constexpr int OFF_VEC = OFF_STG + STG_BYTES;  // LSE2[2][128], Delta[2][128] fp32
+  static constexpr int OFF_RING = 2 * TILE_BYTES;
+  static constexpr int OFF_DS = OFF_RING + RING * TILE_BYTES;  // 128 kv x 128 q 16-bit
+  static constexpr int OFF_STG = OFF_DS + 2 * CHUNK_BYTES;      // dQ boxes 2 x (128 x 32 fp32)
+  static constexpr int OFF_VEC = OFF_STG + 2 * CHUNK_BYTES;     // LSE2[2][128], Delta[2][128]
   static constexpr int OFF_BAR = OFF_VEC + 4 * 512;
-  // kv_full, q_full[2], q_empty[2], s_full, dp_full, pa_full, pb_full, dq_full, dq_free, dkv_full
-  static constexpr int NUM_BARS = 12;
+  // kv_full, ring_full[RING], ring_empty[RING], vec_full[2], vec_empty[2], s_full,
+  // dp_full, pa_full, pb_full, dq_full, dq_free, dkv_full
+  static constexpr int NUM_BARS = 12 + 2 * RING;
   static constexpr int SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr int COL_S = 0, COL_DP = 128, COL_DV = 256, COL_DK = 256 + D;
-  static constexpr int COL_DQ = DQ_T ? COL_DP : 256 + 2 * D;
+  static constexpr int COL_DQ = DQ_IN_DP ? COL_DP : 256 + 2 * D;
 #ifndef FA3B_BWD_EMU128
 #define FA3B_BWD_EMU128 0
 #endif
@@ -192,15 +203,17 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + T::OFF_BAR);
   uint64_t* kv_full = bars;
-  uint64_t* q_full = bars + 1;
-  uint64_t* q_empty = bars + 3;
-  uint64_t* s_full = bars + 5;
-  uint64_t* dp_full = bars + 6;
-  uint64_t* pa_full = bars + 7;
-  uint64_t* pb_full = bars + 8;
-  uint64_t* dq_full = bars + 9;
-  uint64_t* dq_free = bars + 10;
-  uint64_t* dkv_full = bars + 11;
+  uint64_t* ring_full = bars + 1;
+  uint64_t* ring_empty = ring_full + T::RING;
+  uint64_t* vec_full = ring_empty + T::RING;
+  uint64_t* vec_empty = vec_full + 2;
+  uint64_t* s_full = vec_empty + 2;
+  uint64_t* dp_full = s_full + 1;
+  uint64_t* pa_full = s_full + 2;
+  uint64_t* pb_full = s_full + 3;
+  uint64_t* dq_full = s_full + 4;
+  uint64_t* dq_free = s_full + 5;
+  uint64_t* dkv_full = s_full + 6;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + T::NUM_BARS);
   float* lse_s = reinterpret_cast<float*>(smem + T::OFF_VEC);  // [2][128]
   float* del_s = lse_s + 256;                                   // [2][128]
@@ -227,15 +240,22 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
   const int i0 = CAUSAL ? j : 0;
   const int per_head = nq - i0;
   const int n_iter = per_head * args.group;
+  // ring slot and parity of tile t (t = 2i for Q_i, 2i + 1 for dO_i)
+  auto slot_of = [](int t) { return t % T::RING; };
+  auto par_of = [](int t) { return static_cast<uint32_t>((t / T::RING) & 1); };
 
   if (warp == T::MMA_WARP) {
     // the tile offsets above assume a 1024-byte aligned dynamic smem base
     if ((ptx::smem_u32(smem) & 1023u) != 0) __trap();
     if (ptx::lane_id() == 0) {
       ptx::mbar_init(kv_full, 1);
+      for (int s = 0; s < T::RING; ++s) {
+        ptx::mbar_init(&ring_full[s], 1);
+        ptx::mbar_init(&ring_empty[s], 1);
+      }
       for (int s = 0; s < 2; ++s) {
-        ptx::mbar_init(&q_full[s], 1);
-        ptx::mbar_init(&q_empty[s], 1);
+        ptx::mbar_init(&vec_full[s], 1);
+        ptx::mbar_init(&vec_empty[s], 1);
       }
       ptx::mbar_init(s_full, 1);
       ptx::mbar_init(dp_full, 1);
@@ -253,190 +273,212 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+
   // each setmaxnreg dominates the code of its warpgroup's roles
   if (warp >= 12) {
-  if constexpr (T::DQ_T) ptx::setmaxnreg_dec<96>();
-  if (warp == T::LOAD_WARP) {
-    // ------------------------------------------------ TMA producer
-    if (ptx::elect_one()) {
-      ptx::prefetch_tmap(&tmQ);
-      ptx::prefetch_tmap(&tmK);
-      ptx::prefetch_tmap(&tmV);
-      ptx::prefetch_tmap(&tmdO);
-      ptx::mbar_arrive_expect_tx(kv_full, 2 * T::TILE_BYTES);
-      for (int c = 0; c < D / 64; ++c) {
-        ptx::tma_load_4d(smem + T::OFF_K + c * T::CHUNK_BYTES, &tmK, kv_full, c * 64, hkv, j * 128, b,
-                         ptx::kEvictFirst);
-        ptx::tma_load_4d(smem + T::OFF_V + c * T::CHUNK_BYTES, &tmV, kv_full, c * 64, hkv, j * 128, b,
-                         ptx::kEvictFirst);
-      }
-      for (int it = 0; it < n_iter; ++it) {
-        const int s = it & 1;
-        const int h = hkv * args.group + it / per_head;
-        const int i = i0 + it % per_head;
-        const size_t vec = (static_cast<size_t>(b) * args.H + h) * args.Npad + i * 128;
-        ptx::mbar_wait(&q_empty[s], ((it >> 1) & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(&q_full[s], 2 * T::TILE_BYTES + 1024);
+    if constexpr (D == 128) ptx::setmaxnreg_dec<96>();
+    if (warp == T::LOAD_WARP) {
+      // ------------------------------------------------ TMA producer
+      if (ptx::elect_one()) {
+        ptx::prefetch_tmap(&tmQ);
+        ptx::prefetch_tmap(&tmK);
+        ptx::prefetch_tmap(&tmV);
+        ptx::prefetch_tmap(&tmdO);
+        ptx::mbar_arrive_expect_tx(kv_full, 2 * T::TILE_BYTES);
         for (int c = 0; c < D / 64; ++c) {
-          ptx::tma_load_4d(smem + T::OFF_Q + s * T::TILE_BYTES + c * T::CHUNK_BYTES, &tmQ, &q_full[s],
-                           c * 64, h, i * 128, b, ptx::kEvictLast);
-          ptx::tma_load_4d(smem + T::OFF_DO + s * T::TILE_BYTES + c * T::CHUNK_BYTES, &tmdO, &q_full[s],
-                           c * 64, h, i * 128, b, ptx::kEvictLast);
+          ptx::tma_load_4d(smem + T::OFF_K + c * T::CHUNK_BYTES, &tmK, kv_full, c * 64, hkv, j * 128, b,
+                           ptx::kEvictFirst);
+          ptx::tma_load_4d(smem + T::OFF_V + c * T::CHUNK_BYTES, &tmV, kv_full, c * 64, hkv, j * 128, b,
+                           ptx::kEvictFirst);
         }
-        ptx::bulk_load(lse_s + s * 128, args.lse2 + vec, 512, &q_full[s]);
-        ptx::bulk_load(del_s + s * 128, args.delta + vec, 512, &q_full[s]);
+        for (int it = 0; it < n_iter; ++it) {
+          const int h = hkv * args.group + it / per_head;
+          const int i = i0 + it % per_head;
+          const size_t vec = (static_cast<size_t>(b) * args.H + h) * args.Npad + i * 128;
+#pragma unroll
+          for (int which = 0; which < 2; ++which) {  // Q_i then dO_i
+            const int t = 2 * it + which;
+            const int s = slot_of(t);
+            ptx::mbar_wait(&ring_empty[s], par_of(t) ^ 1);
+            const bool vec_here = which == 0 && !T::VEC_OWN;
+            ptx::mbar_arrive_expect_tx(&ring_full[s], T::TILE_BYTES + (vec_here ? 1024 : 0));
+            for (int c = 0; c < D / 64; ++c)
+              ptx::tma_load_4d(smem + T::OFF_RING + s * T::TILE_BYTES + c * T::CHUNK_BYTES,
+                               which ? &tmdO : &tmQ, &ring_full[s], c * 64, h, i * 128, b, ptx::kEvictLast);
+            if (which == 0) {
+              const int vs = it & 1;
+              uint64_t* vbar = &ring_full[s];
+              if (T::VEC_OWN) {
+                ptx::mbar_wait(&vec_empty[vs], ((it >> 1) & 1) ^ 1);
+                ptx::mbar_arrive_expect_tx(&vec_full[vs], 1024);
+                vbar = &vec_full[vs];
+              }
+              ptx::bulk_load(lse_s + vs * 128, args.lse2 + vec, 512, vbar);
+              ptx::bulk_load(del_s + vs * 128, args.delta + vec, 512, vbar);
+            }
+          }
+        }
       }
-    }
-  } else if (warp == T::MMA_WARP) {
-    // ------------------------------------------------ MMA issuer
-    if (ptx::elect_one()) {
-      const uint32_t k_addr = ptx::smem_u32(smem + T::OFF_K);
-      const uint32_t v_addr = ptx::smem_u32(smem + T::OFF_V);
-      const uint32_t ds_addr = ptx::smem_u32(smem + T::OFF_DS);
-      auto q_addr = [&](int s) { return ptx::smem_u32(smem + T::OFF_Q + s * T::TILE_BYTES); };
-      auto do_addr = [&](int s) { return ptx::smem_u32(smem + T::OFF_DO + s * T::TILE_BYTES); };
-      // S^T = K Q^T and dP^T = V dO^T (both operands K-major, 128B swizzle)
-      auto issue_s = [&](int s) {
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off = (k >> 2) * T::CHUNK_BYTES + (k & 3) * 32;
-          ptx::mma_f16_ss(tmem + T::COL_S, ptx::sw128_desc(k_addr + off, 16, 1024),
-                          ptx::sw128_desc(q_addr(s) + off, 16, 1024), idesc_s, k > 0);
-        }
-      };
-      auto issue_dp = [&](int s) {
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off = (k >> 2) * T::CHUNK_BYTES + (k & 3) * 32;
-          ptx::mma_f16_ss(tmem + T::COL_DP, ptx::sw128_desc(v_addr + off, 16, 1024),
-                          ptx::sw128_desc(do_addr(s) + off, 16, 1024), idesc_dp, k > 0);
-        }
-      };
-      ptx::mbar_wait(kv_full, 0);
-      ptx::mbar_wait(&q_full[0], 0);
-      ptx::tc_fence_after();
-      issue_s(0);
-      ptx::mma_commit(s_full);
-      issue_dp(0);
-      ptx::mma_commit(dp_full);
-      for (int it = 0; it < n_iter; ++it) {
-        const int s = it & 1;
-        const bool more = it + 1 < n_iter;
-        // dV += P^T dO (A = P^T pairs in TMEM, B = dO MN-major)
-        ptx::mbar_wait(pa_full, it & 1);
-        BWD_TP(it, 0);
-        ptx::tc_fence_after();
-#pragma unroll
-        for (int t = 0; t < 8; ++t)
-          ptx::mma_f16_ts(tmem + T::COL_DV, tmem + T::COL_S + pair_col(t),
-                          ptx::sw128_desc(do_addr(s) + t * 16 * 128, T::CHUNK_BYTES, 1024), idesc_acc,
-                          (it > 0 || t > 0));
-        // dK += dS^T Q (A = dS^T pairs in TMEM, B = Q MN-major)
-        ptx::mbar_wait(pb_full, it & 1);
-        BWD_TP(it, 1);
-        ptx::tc_fence_after();
-#pragma unroll
-        for (int t = 0; t < 8; ++t)
-          ptx::mma_f16_ts(tmem + T::COL_DK, tmem + T::COL_DP + pair_col(t),
-                          ptx::sw128_desc(q_addr(s) + t * 16 * 128, T::CHUNK_BYTES, 1024), idesc_acc,
-                          (it > 0 || t > 0));
-        ptx::mma_commit(&q_empty[s]);  // Q_i, dO_i, LSE2_i, D_i are consumed
-        if (more) {
-          ptx::mbar_wait(&q_full[s ^ 1], ((it + 1) >> 1) & 1);
+    } else if (warp == T::MMA_WARP) {
+      // ------------------------------------------------ MMA issuer
+      if (ptx::elect_one()) {
+        const uint32_t k_addr = ptx::smem_u32(smem + T::OFF_K);
+        const uint32_t v_addr = ptx::smem_u32(smem + T::OFF_V);
+        const uint32_t ds_addr = ptx::smem_u32(smem + T::OFF_DS);
+        auto tile_addr = [&](int t) { return ptx::smem_u32(smem + T::OFF_RING + slot_of(t) * T::TILE_BYTES); };
+        auto wait_tile = [&](int t) {
+          ptx::mbar_wait(&ring_full[slot_of(t)], par_of(t));
           ptx::tc_fence_after();
-          issue_s(s ^ 1);
-          ptx::mma_commit(s_full);
-        }
-        if (!T::DQ_T && it > 0) {
-          ptx::mbar_wait(dq_free, (it - 1) & 1);
-          ptx::tc_fence_after();
-        }
+        };
+        // S^T = K Q^T and dP^T = V dO^T (both operands K-major, 128B swizzle)
+        auto issue_s = [&](int it) {
+          const uint32_t q_addr = tile_addr(2 * it);
 #pragma unroll
-        for (int t = 0; t < 8; ++t) {  // 16 KV rows per step; every operand MN-major
-          const uint32_t off = t * 16 * 128;
-          if constexpr (T::DQ_T)  // dQ^T = K^T dS^T
-            ptx::mma_f16_ss(tmem + T::COL_DQ, ptx::sw128_desc(k_addr + off, T::CHUNK_BYTES, 1024),
-                            ptx::sw128_desc(ds_addr + off, T::CHUNK_BYTES, 1024), idesc_dq, t > 0);
-          else  // dQ = dS K
-            ptx::mma_f16_ss(tmem + T::COL_DQ, ptx::sw128_desc(ds_addr + off, T::CHUNK_BYTES, 1024),
-                            ptx::sw128_desc(k_addr + off, T::CHUNK_BYTES, 1024), idesc_dq, t > 0);
-        }
-        ptx::mma_commit(dq_full);
-        if (more) {
-          if (T::DQ_T) {  // dP_{i+1} overwrites the dQ_i^T columns once they are drained
-            ptx::mbar_wait(dq_free, it & 1);
+          for (int k = 0; k < D / 16; ++k) {
+            const uint32_t off = (k >> 2) * T::CHUNK_BYTES + (k & 3) * 32;
+            ptx::mma_f16_ss(tmem + T::COL_S, ptx::sw128_desc(k_addr + off, 16, 1024),
+                            ptx::sw128_desc(q_addr + off, 16, 1024), idesc_s, k > 0);
+          }
+        };
+        auto issue_dp = [&](int it) {
+          const uint32_t do_addr = tile_addr(2 * it + 1);
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            const uint32_t off = (k >> 2) * T::CHUNK_BYTES + (k & 3) * 32;
+            ptx::mma_f16_ss(tmem + T::COL_DP, ptx::sw128_desc(v_addr + off, 16, 1024),
+                            ptx::sw128_desc(do_addr + off, 16, 1024), idesc_dp, k > 0);
+          }
+        };
+        ptx::mbar_wait(kv_full, 0);
+        wait_tile(0);
+        issue_s(0);
+        ptx::mma_commit(s_full);
+        wait_tile(1);
+        issue_dp(0);
+        ptx::mma_commit(dp_full);
+        for (int it = 0; it < n_iter; ++it) {
+          const bool more = it + 1 < n_iter;
+          // dV += P^T dO (A = P^T pairs in TMEM, B = dO MN-major); then dO_i is free
+          ptx::mbar_wait(pa_full, it & 1);
+          BWD_TP(it, 0);
+          ptx::tc_fence_after();
+          const uint32_t do_addr = tile_addr(2 * it + 1);
+#pragma unroll
+          for (int t = 0; t < 8; ++t)
+            ptx::mma_f16_ts(tmem + T::COL_DV, tmem + T::COL_S + pair_col(t),
+                            ptx::sw128_desc(do_addr + t * 16 * 128, T::CHUNK_BYTES, 1024), idesc_acc,
+                            (it > 0 || t > 0));
+          if (T::VEC_OWN) ptx::mma_commit(&ring_empty[slot_of(2 * it + 1)]);  // dO_i free early
+          // dK += dS^T Q (A = dS^T pairs in TMEM, B = Q MN-major); then Q_i, LSE2_i, D_i are free
+          ptx::mbar_wait(pb_full, it & 1);
+          BWD_TP(it, 1);
+          ptx::tc_fence_after();
+          const uint32_t q_addr = tile_addr(2 * it);
+#pragma unroll
+          for (int t = 0; t < 8; ++t)
+            ptx::mma_f16_ts(tmem + T::COL_DK, tmem + T::COL_DP + pair_col(t),
+                            ptx::sw128_desc(q_addr + t * 16 * 128, T::CHUNK_BYTES, 1024), idesc_acc,
+                            (it > 0 || t > 0));
+          ptx::mma_commit(&ring_empty[slot_of(2 * it)]);
+          if (T::VEC_OWN)
+            ptx::mma_commit(&vec_empty[it & 1]);
+          else
+            ptx::mma_commit(&ring_empty[slot_of(2 * it + 1)]);
+          if (more) {
+            wait_tile(2 * it + 2);
+            issue_s(it + 1);
+            ptx::mma_commit(s_full);
+          }
+          if (!T::DQ_IN_DP && it > 0) {  // own columns: the previous dQ must have been read out
+            ptx::mbar_wait(dq_free, (it - 1) & 1);
             ptx::tc_fence_after();
           }
-          BWD_TP(it, 2);
-          issue_dp(s ^ 1);
-          ptx::mma_commit(dp_full);
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {  // dQ = dS K: 16 KV rows per step, both operands MN-major
+            const uint32_t off = t * 16 * 128;
+            ptx::mma_f16_ss(tmem + T::COL_DQ, ptx::sw128_desc(ds_addr + off, T::CHUNK_BYTES, 1024),
+                            ptx::sw128_desc(k_addr + off, T::CHUNK_BYTES, 1024), idesc_dq, t > 0);
+          }
+          ptx::mma_commit(dq_full);
+          if (more) {
+            if (T::DQ_IN_DP) {  // dP_{i+1} overwrites the dQ_i columns once they are read out
+              ptx::mbar_wait(dq_free, it & 1);
+              ptx::tc_fence_after();
+            }
+            BWD_TP(it, 2);
+            wait_tile(2 * it + 3);
+            issue_dp(it + 1);
+            ptx::mma_commit(dp_full);
+          }
         }
+        ptx::mma_commit(dkv_full);
       }
-      ptx::mma_commit(dkv_full);
     }
-  }
   } else if (warp >= T::DRAIN_WARP0) {
-    if constexpr (T::DQ_T) ptx::setmaxnreg_inc<160>();
+    if constexpr (D == 128) ptx::setmaxnreg_inc<160>();
     // ------------------------------------------------ dQ writer (the paper's dQ-writer role)
     const int dw = warp - T::DRAIN_WARP0;  // TMEM lane quarter
     const uint32_t lane_base = static_cast<uint32_t>(32 * dw) << 16;
     const int lane = static_cast<int>(ptx::lane_id());
     const bool leader = dw == 0 && lane == 0;
+    const int r = 32 * dw + lane;  // query row of the tile = TMEM lane
+    constexpr int NB = D / 32;     // 128 x 32 fp32 boxes per dQ tile
     for (int it = 0; it < n_iter; ++it) {
       const int h = hkv * args.group + it / per_head;
       const int i = i0 + it % per_head;
-      const size_t row0 = (static_cast<size_t>(b) * args.H + h) * args.Npad + i * 128;
       ptx::mbar_wait(dq_full, it & 1);
       if (dw == 0 && lane == 0) BWD_TP(it, 12);
       ptx::tc_fence_after();
-      if constexpr (T::DQ_T) {
-        uint32_t v[4][32];
+      uint32_t v[NB][32];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) ptx::tmem_ld32(tmem + lane_base + T::COL_DQ + c * 32, v[c]);
-        ptx::tmem_wait_ld();
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(dq_free);
-        if (dw == 0 && lane == 0) BWD_TP(it, 13);
-        // lane = head-dim index 32 dw + lane; register (c, e) = query row 32 c + e
-        float* dst = args.dq_acc + row0 * D + 32 * dw + lane;
-#ifndef FA3B_BWD_NO_RED  // diagnosis builds only: drop the dQ reduction
+      for (int c = 0; c < NB; ++c) ptx::tmem_ld32(tmem + lane_base + T::COL_DQ + c * 32, v[c]);
+      ptx::tmem_wait_ld();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(dq_free);
+      if (dw == 0 && lane == 0) BWD_TP(it, 13);
+      if constexpr (D == 128) {
+        // four boxes through two staging buffers: each buffer is refilled once the
+        // reduce-add issued two boxes earlier has finished reading it
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-#pragma unroll
-          for (int e = 0; e < 32; ++e) ptx::red_add_f32(dst + (32 * c + e) * D, __uint_as_float(v[c][e]));
-#else
-        if (v[0][0] == 0x7fffffffu && dst == nullptr) ptx::red_add_f32(dst, 0.f);
-#endif
-      } else {
-        uint32_t v[2][32];
-#pragma unroll
-        for (int c = 0; c < 2; ++c) ptx::tmem_ld32(tmem + lane_base + T::COL_DQ + c * 32, v[c]);
-        ptx::tmem_wait_ld();
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(dq_free);
-        // query row r = TMEM lane; two 128 x 32 fp32 boxes, 128B-swizzled like the TMA map
-        if (leader) ptx::bulk_wait_group_read<0>();
-        ptx::named_bar_sync(3, 128);
-        const int r = 32 * dw + lane;
-        uint8_t* stg = smem + T::OFF_STG + r * 128;
-#pragma unroll
-        for (int bx = 0; bx < 2; ++bx)
+        for (int c = 0; c < NB; ++c) {
+          if (leader && (it > 0 || c >= 2)) ptx::bulk_wait_group_read<1>();
+          ptx::named_bar_sync(3, 128);
+          uint8_t* stg = smem + T::OFF_STG + (c & 1) * T::CHUNK_BYTES + r * 128;
 #pragma unroll
           for (int u = 0; u < 8; ++u)
-            *reinterpret_cast<uint4*>(stg + bx * T::CHUNK_BYTES + ((u ^ (r & 7)) << 4)) =
-                make_uint4(v[bx][4 * u], v[bx][4 * u + 1], v[bx][4 * u + 2], v[bx][4 * u + 3]);
+            *reinterpret_cast<uint4*>(stg + ((u ^ (r & 7)) << 4)) =
+                make_uint4(v[c][4 * u], v[c][4 * u + 1], v[c][4 * u + 2], v[c][4 * u + 3]);
+          ptx::fence_proxy_async_smem();
+          ptx::named_bar_sync(3, 128);
+          if (leader) {
+            ptx::tma_reduce_add_4d(&tmDQ, smem + T::OFF_STG + (c & 1) * T::CHUNK_BYTES, 32 * c, h, i * 128, b);
+            ptx::bulk_commit_group();
+          }
+        }
+      } else {
+        // both boxes at once, after the previous tile's reduce-adds have read them
+        if (leader) ptx::bulk_wait_group_read<0>();
+        ptx::named_bar_sync(3, 128);
+#pragma unroll
+        for (int c = 0; c < NB; ++c) {
+          uint8_t* stg = smem + T::OFF_STG + c * T::CHUNK_BYTES + r * 128;
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            *reinterpret_cast<uint4*>(stg + ((u ^ (r & 7)) << 4)) =
+                make_uint4(v[c][4 * u], v[c][4 * u + 1], v[c][4 * u + 2], v[c][4 * u + 3]);
+        }
         ptx::fence_proxy_async_smem();
         ptx::named_bar_sync(3, 128);
         if (leader) {
-          ptx::tma_reduce_add_4d(&tmDQ, smem + T::OFF_STG, 0, h, i * 128, b);
-          ptx::tma_reduce_add_4d(&tmDQ, smem + T::OFF_STG + T::CHUNK_BYTES, 32, h, i * 128, b);
+#pragma unroll
+          for (int c = 0; c < NB; ++c)
+            ptx::tma_reduce_add_4d(&tmDQ, smem + T::OFF_STG + c * T::CHUNK_BYTES, 32 * c, h, i * 128, b);
           ptx::bulk_commit_group();
         }
       }
     }
-    if (!T::DQ_T && leader) ptx::bulk_wait_group<0>();
+    if (leader) ptx::bulk_wait_group<0>();
   } else {
     // ------------------------------------------------ 2 gradient warpgroups
     const int w = warp >> 2;          // which 64-column half of the query tile
@@ -458,6 +500,7 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
       uint32_t sr[64];
       ptx::tmem_ld32(tmem + lane_base + T::COL_S + 64 * w, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
       ptx::tmem_ld32(tmem + lane_base + T::COL_S + 64 * w + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+      if (T::VEC_OWN) ptx::mbar_wait(&vec_full[s], (it >> 1) & 1);
       ptx::tmem_wait_ld();
       const bool diag = CAUSAL && i == j;
       const int lim = kv_row - (i * 128 + 64 * w);  // causal: query column c is visible iff c >= lim
@@ -504,7 +547,6 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
         uint32_t dpr[32];
         ptx::tmem_ld32(tmem + lane_base + T::COL_DP + 64 * w + 32 * hf, dpr);
         ptx::tmem_wait_ld();
-        if (trc && w == 0) BWD_TP(it, hf ? 15 : 3);
         uint32_t dk2[16];
 #pragma unroll
         for (int c4 = 0; c4 < 8; ++c4) {
@@ -528,7 +570,6 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
           *reinterpret_cast<uint4*>(ds_row + ((uu ^ (r & 7)) << 4)) =
               make_uint4(dk2[4 * u], dk2[4 * u + 1], dk2[4 * u + 2], dk2[4 * u + 3]);
         }
-        if (trc && w == 0 && hf == 0) BWD_TP(it, 14);
       }
       ptx::fence_proxy_async_smem();
       ptx::tmem_wait_st();
@@ -640,9 +681,8 @@ int launch_bwd_main(const fa3b_bwd_params& p, const Workspace& ws, int Npad, cud
   const uint32_t idesc_s = ptx::make_idesc(128, 128, fmt, fmt, false, false, p.alpha < 0);
   const uint32_t idesc_dp = ptx::make_idesc(128, 128, fmt, fmt, false, false, false);
   const uint32_t idesc_acc = ptx::make_idesc(128, D, fmt, fmt, false, true, false);
-  // dQ^T = K^T dS^T (M = D = 128) or dQ = dS K (M = 128 query rows, N = D = 64); all MN-major
-  const uint32_t idesc_dq = Tr::DQ_T ? ptx::make_idesc(128, 128, fmt, fmt, true, true, false)
-                                     : ptx::make_idesc(128, D, fmt, fmt, true, true, false);
+  // dQ = dS K (M = 128 query rows, N = D), both operands MN-major
+  const uint32_t idesc_dq = ptx::make_idesc(128, D, fmt, fmt, true, true, false);
   dim3 grid(Npad / 128, p.heads_kv, p.batch);
   kern<<<grid, Tr::NUM_THREADS, Tr::SMEM_BYTES, st>>>(tq, tk, tv, tdo, tdq, a, idesc_s, idesc_dp, idesc_acc,
                                                       idesc_dq);
