@@ -183,6 +183,9 @@ struct BwdTraits {
 #ifndef FA3B_BWD_EMU128
 #define FA3B_BWD_EMU128 0
 #endif
+#ifndef FA3B_BWD_S_EARLY
+#define FA3B_BWD_S_EARLY 1
+#endif
   // exp2 pairs (of every 8) evaluated on the FMA-pipe polynomial instead of MUFU.EX2
   static constexpr int EMU = D == 64 ? 2 : FA3B_BWD_EMU128;
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
@@ -369,6 +372,15 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
                             ptx::sw128_desc(do_addr + t * 16 * 128, T::CHUNK_BYTES, 1024), idesc_acc,
                             (it > 0 || t > 0));
           if (T::VEC_OWN) ptx::mma_commit(&ring_empty[slot_of(2 * it + 1)]);  // dO_i free early
+#if FA3B_BWD_S_EARLY
+          // S_{i+1} may overwrite the S^T columns as soon as dV_i (the last reader of
+          // P_i^T) is issued: phase A of tile i+1 then overlaps phase B of tile i
+          if (more) {
+            wait_tile(2 * it + 2);
+            issue_s(it + 1);
+            ptx::mma_commit(s_full);
+          }
+#endif
           // dK += dS^T Q (A = dS^T pairs in TMEM, B = Q MN-major); then Q_i, LSE2_i, D_i are free
           ptx::mbar_wait(pb_full, it & 1);
           BWD_TP(it, 1);
@@ -384,11 +396,13 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
             ptx::mma_commit(&vec_empty[it & 1]);
           else
             ptx::mma_commit(&ring_empty[slot_of(2 * it + 1)]);
+#if !FA3B_BWD_S_EARLY
           if (more) {
             wait_tile(2 * it + 2);
             issue_s(it + 1);
             ptx::mma_commit(s_full);
           }
+#endif
           if (!T::DQ_IN_DP && it > 0) {  // own columns: the previous dQ must have been read out
             ptx::mbar_wait(dq_free, (it - 1) & 1);
             ptx::tc_fence_after();

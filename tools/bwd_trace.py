@@ -25,6 +25,6 @@ per = np.diff(t[8:60, 0])
 print(f"mean cycles between pa_seen = {per.mean():.0f}  (5 GEMMs = {5 * 128 * 128 * D // 8192 * 2} tensor cycles)")
 d = t[8:60]
 def m(a, b): return np.mean(d[:, b] - d[:, a])
-print(f"B sub-phases (c0): dp_seen->ld0 {m(6,3):.0f} | ld0->hf0 done {m(3,14):.0f} | ->ld1 {m(14,15):.0f} | ld1->B_done {m(15,7):.0f}")
+
 print(f"A phase (s_seen->A_done) {m(4,5):.0f} | B phase (dp_seen->B_done) {m(6,7):.0f} | A_done->pa_seen {m(5,0):.0f} | "
       f"B_done->pb_seen {m(7,1):.0f} | dq_seen->dq_free {m(12,13):.0f} | dq_free->mma seen {m(13,2):.0f}")
