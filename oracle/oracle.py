@@ -23,6 +23,7 @@ import numpy as np
 HERE = Path(__file__).resolve().parent
 PORT_LIB = HERE / "_build" / "libfa3b_oracle.so"
 REF_LIB = HERE / "_ref" / "libflashlab_ref.so"
+REF_SIM = HERE / "_ref" / "flashlab_sim"
 REF_SRC = Path(os.environ.get("FLASHLAB_REF_DIR", "/root/reference/proj/core"))
 
 FP64, FP32, FP16, BF16, E4M3 = 0, 1, 2, 3, 4
@@ -258,6 +259,7 @@ class Ref(_Base):
         self._check(self.fn("sign_vector", [_SZ, _U64, _D])(n, seed, _dp(out)))
         return out
 
+
     def round_to(self, x, fmt, overflow_infinite=False):
         return float(self.fn("round_to", [_DBL, _I, _I], _DBL)(float(x), fmt,
                                                               int(overflow_infinite)))
@@ -388,3 +390,19 @@ class Ref(_Base):
         out = (ctypes.c_uint64 * max(width, 1))()
         self._check(self.fn("accumulator_permutation", [_SZ, _U64P])(width, out))
         return [int(x) for x in out[:width]]
+
+
+def simulate(model_path, *, seqlen=8192, headdim=128, block_rows=128, block_cols=128,
+             backward=False, fp8=False, schedule="pingpong+2stage") -> dict:
+    """The reference's discrete-event schedule model (pipeline_sim.hpp) run by
+    _ref/flashlab_sim (a subprocess: the simulator's iostream code and numpy's
+    runtime libraries do not share one process)."""
+    if not REF_SIM.exists():
+        build()
+    args = [str(REF_SIM), str(model_path), str(seqlen), str(headdim), str(block_rows),
+            str(block_cols), str(int(backward)), str(int(fp8)), schedule]
+    r = subprocess.run(args, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise OracleError(r.stderr.strip() or r.stdout.strip())
+    import json
+    return json.loads(r.stdout)
