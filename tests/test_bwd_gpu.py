@@ -65,6 +65,9 @@ CASES = [
     pytest.param(2, 2, 1, 300, 128, False, "fp16", None, id="gqa-ragged-fp16"),
     pytest.param(1, 4, 2, 200, 64, True, "bf16", -0.11, id="neg-alpha-causal-gqa"),
     pytest.param(1, 1, 1, 1000, 128, True, "bf16", None, id="ragged-1000"),
+    # long GQA groups: the Q/dO ring and the LSE/D buffers wrap many times within a CTA
+    pytest.param(1, 8, 1, 640, 128, True, "bf16", None, id="gqa8-ring-d128"),
+    pytest.param(1, 4, 1, 520, 64, False, "fp16", None, id="gqa4-ring-d64"),
 ]
 
 
