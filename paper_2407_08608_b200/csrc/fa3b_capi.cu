@@ -6,6 +6,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -43,6 +44,19 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
+// Ping-pong pairing choice; FA3B_FWD_PAIRING=cta|warp overrides the measured default.
+bool fwd_pairing_impl(int head_dim, bool causal, bool fp8) {
+  static const int forced = [] {
+    const char* e = std::getenv("FA3B_FWD_PAIRING");
+    if (e == nullptr) return -1;
+    return std::strcmp(e, "cta") == 0 ? 1 : (std::strcmp(e, "warp") == 0 ? 0 : -1);
+  }();
+  (void)causal;
+  (void)fp8;
+  if (head_dim > 128) return false;
+  return forced == 1;  // warp pairing measured faster on every C2/C3/C5 shape
+}
+
 int check_device() {
   static int status = [] {
     int dev = 0;
@@ -57,6 +71,8 @@ int check_device() {
 }
 
 }  // namespace
+
+bool fwd_pairing(int head_dim, bool causal, bool fp8) { return fwd_pairing_impl(head_dim, causal, fp8); }
 
 // [batch, seq, head, dim] tensor -> 4D map (dim, head, seq, batch) with a box
 // of (inner_elems, 1, rows, 1) and 128B swizzle. OOB rows read as zero.
@@ -108,10 +124,10 @@ int validate_problem(int batch, int heads_q, int heads_kv, int seqlen, int head_
 
 namespace {
 
-template <int D, int NT, bool CAUSAL, bool BF16>
+template <int D, int NT, bool CAUSAL, bool BF16, int CPS>
 int launch_fwd16(const fa3b_fwd_params& p, cudaStream_t stream) {
-  using T = FwdTraits<D, NT>;
-  auto kern = fa3b_fwd_kernel<D, NT, CAUSAL, BF16 ? KIND_BF16 : KIND_F16>;
+  using T = FwdTraits<D, NT, 2, CPS>;
+  auto kern = fa3b_fwd_kernel<D, NT, CAUSAL, BF16 ? KIND_BF16 : KIND_F16, CPS>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
@@ -157,12 +173,12 @@ int launch_fwd16(const fa3b_fwd_params& p, cudaStream_t stream) {
   return FA3B_OK;
 }
 
-template <int D, int NT>
+template <int D, int NT, int CPS = 1>
 int launch_fwd16_dt(const fa3b_fwd_params& p, cudaStream_t s) {
   const bool bf16 = p.in_dtype == FA3B_DTYPE_BF16;
   if (p.causal)
-    return bf16 ? launch_fwd16<D, NT, true, true>(p, s) : launch_fwd16<D, NT, true, false>(p, s);
-  return bf16 ? launch_fwd16<D, NT, false, true>(p, s) : launch_fwd16<D, NT, false, false>(p, s);
+    return bf16 ? launch_fwd16<D, NT, true, true, CPS>(p, s) : launch_fwd16<D, NT, true, false, CPS>(p, s);
+  return bf16 ? launch_fwd16<D, NT, false, true, CPS>(p, s) : launch_fwd16<D, NT, false, false, CPS>(p, s);
 }
 
 }  // namespace
@@ -248,9 +264,17 @@ int fa3b_fwd(const fa3b_fwd_params* pp) {
   cudaStream_t s = static_cast<cudaStream_t>(p.stream);
   if (fp8) return launch_fwd_fp8(p, s);
   const bool basic = p.schedule == FA3B_SCHED_BASIC;
+  // Ping-pong pairs: two query tiles of one CTA (warp pairing, the default) or
+  // one tile in each of two CTAs per SM (CTA pairing, FA3B_FWD_PAIRING=cta);
+  // A/B in profiles/r01m_pairing_ab.log.
+  const bool cta_pairs = fwd_pairing(p.head_dim, p.causal != 0, false);
   switch (p.head_dim) {
-    case 64: return basic ? launch_fwd16_dt<64, 1>(p, s) : launch_fwd16_dt<64, 2>(p, s);
-    case 128: return basic ? launch_fwd16_dt<128, 1>(p, s) : launch_fwd16_dt<128, 2>(p, s);
+    case 64:
+      return basic ? launch_fwd16_dt<64, 1>(p, s)
+                   : (cta_pairs ? launch_fwd16_dt<64, 1, 2>(p, s) : launch_fwd16_dt<64, 2>(p, s));
+    case 128:
+      return basic ? launch_fwd16_dt<128, 1>(p, s)
+                   : (cta_pairs ? launch_fwd16_dt<128, 1, 2>(p, s) : launch_fwd16_dt<128, 2>(p, s));
     case 256: return launch_fwd16_dt<256, 1>(p, s);
   }
   return FA3B_ERR_HEAD_DIM;

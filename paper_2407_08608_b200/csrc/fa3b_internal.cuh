@@ -20,5 +20,7 @@ int validate_problem(int batch, int heads_q, int heads_kv, int seqlen, int head_
                      double alpha);
 
 int launch_fwd_fp8(const fa3b_fwd_params& p, cudaStream_t stream);
+// true: pair query tiles across two CTAs per SM; false: two tiles in one CTA
+bool fwd_pairing(int head_dim, bool causal, bool fp8);
 
 }  // namespace fa3b

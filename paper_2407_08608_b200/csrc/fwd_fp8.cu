@@ -29,10 +29,10 @@ float fp8_threshold(bool kv_blocked) {
   return kv_blocked ? 0.f : 4.f;
 }
 
-template <int D, int NT, bool CAUSAL>
+template <int D, int NT, bool CAUSAL, int CPS = 1>
 int launch(const fa3b_fwd_params& p, cudaStream_t stream) {
-  using T = FwdTraits<D, NT, 1>;
-  auto kern = fa3b_fwd_kernel<D, NT, CAUSAL, KIND_E4M3>;
+  using T = FwdTraits<D, NT, 1, CPS>;
+  auto kern = fa3b_fwd_kernel<D, NT, CAUSAL, KIND_E4M3, CPS>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
@@ -82,9 +82,14 @@ int launch_fwd_fp8(const fa3b_fwd_params& p, cudaStream_t s) {
     return FA3B_ERR_BLOCK;
   const bool basic = p.schedule == FA3B_SCHED_BASIC;
   switch (p.head_dim) {
-    case 128:
-      if (p.causal) return basic ? launch<128, 1, true>(p, s) : launch<128, 2, true>(p, s);
-      return basic ? launch<128, 1, false>(p, s) : launch<128, 2, false>(p, s);
+    case 128: {
+      const bool cta_pairs = fwd_pairing(128, p.causal != 0, true);
+      if (p.causal)
+        return basic ? launch<128, 1, true>(p, s)
+                     : (cta_pairs ? launch<128, 1, true, 2>(p, s) : launch<128, 2, true>(p, s));
+      return basic ? launch<128, 1, false>(p, s)
+                   : (cta_pairs ? launch<128, 1, false, 2>(p, s) : launch<128, 2, false>(p, s));
+    }
     case 256:
       return p.causal ? launch<256, 1, true>(p, s) : launch<256, 1, false>(p, s);
   }

@@ -102,23 +102,28 @@ struct FwdArgs {
   float fp8_thr;         // lazy-rescale threshold (log2) for the e4m3 P
 };
 
-template <int D_, int NT_, int EB_ = 2>
+// CPS_ = CTAs per SM. CPS = 2 (one query tile per CTA, d <= 128) gives the
+// tensor core two independent tiles per SM from two CTAs instead of one CTA's
+// ping-pong pair: half the TMEM (256 columns) and fewer K/V stages each.
+template <int D_, int NT_, int EB_ = 2, int CPS_ = 1>
 struct FwdTraits {
   static constexpr int D = D_;
   static constexpr int NT = NT_;
   static constexpr int EB = EB_;  // bytes per element (2 f16/bf16, 1 e4m3)
+  static constexpr int CPS = CPS_;
   static constexpr int BM = 128;
   static constexpr int BN = 128;
   static constexpr int CHUNK_BYTES = 128 * 128;  // 128 rows x 128 bytes
   static constexpr int CHUNK_ELEMS = 128 / EB;
   static constexpr int CHUNKS = D / CHUNK_ELEMS;
   static constexpr int TILE_BYTES = CHUNKS * CHUNK_BYTES;
-  static constexpr int STAGES = TILE_BYTES <= 16384 ? 8 : (TILE_BYTES <= 32768 ? 4 : 2);
+  static constexpr int STAGES = CPS == 2 ? (TILE_BYTES <= 16384 ? 4 : 2)
+                                         : (TILE_BYTES <= 16384 ? 8 : (TILE_BYTES <= 32768 ? 4 : 2));
   // two softmax warpgroups per query tile, each owning 64 of the 128 columns
   static constexpr int NUM_THREADS = NT * 256 + 64;
   static constexpr int LOAD_WARP = NT * 8;
   static constexpr int MMA_WARP = NT * 8 + 1;
-  static constexpr uint32_t TMEM_COLS = 512;
+  static constexpr uint32_t TMEM_COLS = CPS == 2 ? 256 : 512;
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_KV = NT * TILE_BYTES;
   static constexpr int OFF_BAR = OFF_KV + STAGES * TILE_BYTES;
@@ -127,7 +132,8 @@ struct FwdTraits {
   // row-max / row-sum exchange between the two column halves: [NT][2 buf][2 half][128]
   static constexpr int OFF_XCH = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr int SMEM_BYTES = OFF_XCH + NT * 2 * 2 * 128 * 4 + 1024;
-  static_assert(NT * (128 + D) <= 512, "TMEM budget");
+  static_assert(NT * (128 + D) <= static_cast<int>(TMEM_COLS), "TMEM budget");
+  static_assert(CPS == 1 || (NT == 1 && SMEM_BYTES * 2 <= 233472), "two CTAs per SM");
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
   __host__ __device__ static constexpr int s_col(int t) { return t * 128; }
   __host__ __device__ static constexpr int o_col(int t) { return NT * 128 + t * D; }
@@ -138,15 +144,15 @@ struct FwdTraits {
 #define FA3B_FWD_EMU 2
 #endif
 
-template <int D, int NT, bool CAUSAL, int KIND, int EMU = FA3B_FWD_EMU>
-__global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2>::NUM_THREADS, 1)
+template <int D, int NT, bool CAUSAL, int KIND, int CPS = 1, int EMU = FA3B_FWD_EMU>
+__global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CPS>::NUM_THREADS, CPS)
     fa3b_fwd_kernel(const __grid_constant__ CUtensorMap tmQ,
                     const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const FwdArgs args,
                     const uint32_t idesc_qk, const uint32_t idesc_pv) {
   constexpr bool FP8 = KIND == KIND_E4M3;
   constexpr bool BF16 = KIND == KIND_BF16;
-  using T = FwdTraits<D, NT, FP8 ? 1 : 2>;
+  using T = FwdTraits<D, NT, FP8 ? 1 : 2, CPS>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
