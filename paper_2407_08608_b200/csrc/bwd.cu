@@ -655,14 +655,9 @@ template <int D, bool CAUSAL, bool BF16>
 int launch_bwd_main(const fa3b_bwd_params& p, const Workspace& ws, int Npad, cudaStream_t st) {
   using Tr = BwdTraits<D>;
   auto kern = fa3b_bwd_kernel<D, CAUSAL, BF16>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Tr::SMEM_BYTES);
-  });
-  if (attr_err != cudaSuccess) return cuda_fail(attr_err);
+  int rc = ensure_smem_attr(reinterpret_cast<const void*>(kern), Tr::SMEM_BYTES);
+  if (rc != FA3B_OK) return rc;
   CUtensorMap tq, tk, tv, tdo;
-  int rc;
   if ((rc = make_tmap_4d(&tq, p.q, 2, D, p.heads_q, p.seqlen, p.batch, 64, 128)) != FA3B_OK) return rc;
   if ((rc = make_tmap_4d(&tk, p.k, 2, D, p.heads_kv, p.seqlen, p.batch, 64, 128)) != FA3B_OK) return rc;
   if ((rc = make_tmap_4d(&tv, p.v, 2, D, p.heads_kv, p.seqlen, p.batch, 64, 128)) != FA3B_OK) return rc;

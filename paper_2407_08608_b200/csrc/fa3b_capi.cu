@@ -9,6 +9,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <utility>
+#include <vector>
 
 #include "../../include/fa3b.h"
 #include "fa3b_internal.cuh"
@@ -74,6 +76,21 @@ int check_device() {
 
 bool fwd_pairing(int head_dim, bool causal, bool fp8) { return fwd_pairing_impl(head_dim, causal, fp8); }
 
+int ensure_smem_attr(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> done;  // (kernel, device)
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e);
+  std::lock_guard<std::mutex> lock(mu);
+  for (const auto& d : done)
+    if (d.first == kernel && d.second == dev) return FA3B_OK;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return cuda_fail(e);
+  done.emplace_back(kernel, dev);
+  return FA3B_OK;
+}
+
 // [batch, seq, head, dim] tensor -> 4D map (dim, head, seq, batch) with a box
 // of (inner_elems, 1, rows, 1) and 128B swizzle. OOB rows read as zero.
 int make_tmap_4d(CUtensorMap* map, const fa3b_tensor4& t, int elem_bytes, int dim, int heads,
@@ -128,16 +145,10 @@ template <int D, int NT, bool CAUSAL, bool BF16, int CPS>
 int launch_fwd16(const fa3b_fwd_params& p, cudaStream_t stream) {
   using T = FwdTraits<D, NT, 2, CPS>;
   auto kern = fa3b_fwd_kernel<D, NT, CAUSAL, BF16 ? KIND_BF16 : KIND_F16, CPS>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    T::SMEM_BYTES);
-  });
-  if (attr_err != cudaSuccess) return cuda_fail(attr_err);
+  int rc = ensure_smem_attr(reinterpret_cast<const void*>(kern), T::SMEM_BYTES);
+  if (rc != FA3B_OK) return rc;
 
   CUtensorMap tq, tk, tv;
-  int rc;
   if ((rc = make_tmap_4d(&tq, p.q, 2, D, p.heads_q, p.seqlen, p.batch, 64, 128)) != FA3B_OK)
     return rc;
   if ((rc = make_tmap_4d(&tk, p.k, 2, D, p.heads_kv, p.seqlen, p.batch, 64, 128)) != FA3B_OK)

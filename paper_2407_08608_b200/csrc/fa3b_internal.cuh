@@ -20,6 +20,10 @@ int validate_problem(int batch, int heads_q, int heads_kv, int seqlen, int head_
                      double alpha);
 
 int launch_fwd_fp8(const fa3b_fwd_params& p, cudaStream_t stream);
+// Raise a kernel's dynamic shared-memory limit once per (kernel, device): the
+// attribute belongs to the function as loaded on the current device, so a
+// process driving several GPUs needs it on each.
+int ensure_smem_attr(const void* kernel, int bytes);
 // true: pair query tiles across two CTAs per SM; false: two tiles in one CTA
 bool fwd_pairing(int head_dim, bool causal, bool fp8);
 

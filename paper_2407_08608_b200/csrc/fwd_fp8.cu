@@ -33,14 +33,9 @@ template <int D, int NT, bool CAUSAL, int CPS = 1>
 int launch(const fa3b_fwd_params& p, cudaStream_t stream) {
   using T = FwdTraits<D, NT, 1, CPS>;
   auto kern = fa3b_fwd_kernel<D, NT, CAUSAL, KIND_E4M3, CPS>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM_BYTES);
-  });
-  if (attr_err != cudaSuccess) return cuda_fail(attr_err);
+  int rc = ensure_smem_attr(reinterpret_cast<const void*>(kern), T::SMEM_BYTES);
+  if (rc != FA3B_OK) return rc;
   CUtensorMap tq, tk, tv;
-  int rc;
   if ((rc = make_tmap_4d(&tq, p.q, 1, D, p.heads_q, p.seqlen, p.batch, 128, 128)) != FA3B_OK) return rc;
   if ((rc = make_tmap_4d(&tk, p.k, 1, D, p.heads_kv, p.seqlen, p.batch, 128, 128)) != FA3B_OK) return rc;
   if ((rc = make_tmap_4d(&tv, p.v, 1, D, p.heads_kv, p.seqlen, p.batch, 128, 128)) != FA3B_OK) return rc;
