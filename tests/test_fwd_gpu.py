@@ -176,6 +176,32 @@ def test_full_size_against_torch_rows(cuda, D, causal):
         assert (lse[0, h, rows] - ref_l).abs().max().item() < 1e-3
 
 
+@pytest.mark.parametrize("B,N,H,Hkv,causal", [(1, 65536, 1, 1, True), (1, 8192, 64, 8, False),
+                                              (64, 256, 8, 8, True)])
+def test_extreme_shapes_against_torch_rows(cuda, B, N, H, Hkv, causal):
+    """64k keys (qb grid and LPT order at their largest), C5's 64/8 GQA, and a
+    4096-tile batch x head grid: sampled rows against fp32 torch."""
+    api = _api()
+    torch = _torch()
+    D = 128
+    gen = torch.Generator(device="cuda").manual_seed(N + H)
+    q = torch.randn(B, N, H, D, device="cuda", generator=gen, dtype=torch.bfloat16)
+    k, v = (torch.randn(B, N, Hkv, D, device="cuda", generator=gen, dtype=torch.bfloat16)
+            for _ in range(2))
+    o, lse = api.fwd(q, k, v, causal=causal)
+    alpha = 1 / math.sqrt(D)
+    rows = torch.unique(torch.cat([torch.tensor([0, 1, N - 1]),
+                                   torch.randint(0, N, (61,), generator=gen, device="cuda").cpu()])).cuda()
+    for b in sorted({0, B - 1}):
+        for h in sorted({0, H // 2, H - 1}):
+            kh = h // (H // Hkv)
+            s = alpha * q[b, rows, h].float() @ k[b, :, kh].float().T
+            if causal:
+                s = s.masked_fill(torch.arange(N, device="cuda")[None, :] > rows[:, None], -math.inf)
+            assert (o[b, rows, h].float() - torch.softmax(s, -1) @ v[b, :, kh].float()).abs().max().item() < 2e-2
+            assert (lse[b, h, rows] - torch.logsumexp(s, -1)).abs().max().item() < 1e-3
+
+
 def test_fwd_rejects_bad_arguments(cuda):
     api = _api()
     torch = _torch()
