@@ -76,6 +76,21 @@ int check_device() {
 
 bool fwd_pairing(int head_dim, bool causal, bool fp8) { return fwd_pairing_impl(head_dim, causal, fp8); }
 
+int num_sms() {
+  static std::mutex mu;
+  static std::vector<int> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev >= static_cast<int>(cache.size())) cache.resize(dev + 1, 0);
+  if (cache[dev] == 0) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n > 0 ? n : 148;
+  }
+  return cache[dev];
+}
+
 int ensure_smem_attr(const void* kernel, int bytes) {
   static std::mutex mu;
   static std::vector<std::pair<const void*, int>> done;  // (kernel, device)
@@ -176,7 +191,7 @@ int launch_fwd16(const fa3b_fwd_params& p, cudaStream_t stream) {
   const uint32_t idesc_qk = ptx::make_idesc(128, 128, fmt, fmt, false, false, p.alpha < 0);
   const uint32_t idesc_pv = ptx::make_idesc(128, D, fmt, fmt, false, true, false);
 
-  dim3 grid((p.seqlen + NT * 128 - 1) / (NT * 128), p.heads_q, p.batch);
+  const int grid = fwd_grid(p.seqlen, NT, p.heads_q, p.batch, CPS);  // persistent CTAs
   kern<<<grid, T::NUM_THREADS, T::SMEM_BYTES, stream>>>(tq, tk, tv, a, idesc_qk, idesc_pv);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e);

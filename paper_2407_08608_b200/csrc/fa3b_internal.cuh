@@ -24,6 +24,14 @@ int launch_fwd_fp8(const fa3b_fwd_params& p, cudaStream_t stream);
 // attribute belongs to the function as loaded on the current device, so a
 // process driving several GPUs needs it on each.
 int ensure_smem_attr(const void* kernel, int bytes);
+// Streaming multiprocessors of the current device (cached per device).
+int num_sms();
+// Persistent forward grid: one CTA per SM (or per SM slot), never more than the work.
+inline int fwd_grid(int seqlen, int nt, int heads, int batch, int ctas_per_sm) {
+  const long long items = static_cast<long long>((seqlen + nt * 128 - 1) / (nt * 128)) * heads * batch;
+  const long long cap = static_cast<long long>(num_sms()) * ctas_per_sm;
+  return static_cast<int>(items < cap ? items : cap);
+}
 // true: pair query tiles across two CTAs per SM; false: two tiles in one CTA
 bool fwd_pairing(int head_dim, bool causal, bool fp8);
 

@@ -60,7 +60,7 @@ int launch(const fa3b_fwd_params& p, cudaStream_t stream) {
   a.fp8_thr = fp8_threshold(a.kv_blocked != 0);
   const uint32_t idesc_qk = ptx::make_idesc(128, 128, 0, 0, false, false, p.alpha < 0);
   const uint32_t idesc_pv = ptx::make_idesc(128, D, 0, 0, false, true, false);
-  dim3 grid((p.seqlen + NT * 128 - 1) / (NT * 128), p.heads_q, p.batch);
+  const int grid = fwd_grid(p.seqlen, NT, p.heads_q, p.batch, CPS);  // persistent CTAs
   kern<<<grid, T::NUM_THREADS, T::SMEM_BYTES, stream>>>(tq, tk, tv, a, idesc_qk, idesc_pv);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e);

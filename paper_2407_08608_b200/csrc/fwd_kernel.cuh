@@ -127,8 +127,8 @@ struct FwdTraits {
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_KV = NT * TILE_BYTES;
   static constexpr int OFF_BAR = OFF_KV + STAGES * TILE_BYTES;
-  // q_full, kv_full[S], kv_empty[S], s_full[NT], p_full[NT], o_full[NT]
-  static constexpr int NUM_BARS = 1 + 2 * STAGES + 3 * NT;
+  // q_full, kv_full[S], kv_empty[S], s_full[NT], p_full[NT], o_full[NT], q_empty
+  static constexpr int NUM_BARS = 2 + 2 * STAGES + 3 * NT;
   // row-max / row-sum exchange between the two column halves: [NT][2 buf][2 half][128]
   static constexpr int OFF_XCH = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr int SMEM_BYTES = OFF_XCH + NT * 2 * 2 * 128 * 4 + 1024;
@@ -163,6 +163,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
   uint64_t* s_full = kv_empty + T::STAGES;
   uint64_t* p_full = s_full + NT;
   uint64_t* o_full = p_full + NT;
+  uint64_t* q_empty = o_full + NT;  // the Q tiles of a work item are consumed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + T::NUM_BARS);
 
   const int warp = static_cast<int>(ptx::warp_id());
@@ -172,37 +173,42 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
     FA3B_CTA(1, fa3b_smid());
   }
 #endif
-  const int nqb = gridDim.x;
-#ifndef FA3B_CAUSAL_LPT
-#define FA3B_CAUSAL_LPT 1
-#endif
-  // Non-causal: query blocks of one head are adjacent in launch order (K/V reuse in L2).
-  // Causal: launch order is longest-first across all heads (the linear block index
-  // walks the query blocks from the bottom of the mask up, every head at each step).
-  int qb, h, b;
-  if (CAUSAL && FA3B_CAUSAL_LPT) {
-    const int lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-    const int hb = gridDim.y * gridDim.z;
-    qb = nqb - 1 - lin / hb;
-    h = (lin % hb) % gridDim.y;
-    b = (lin % hb) / gridDim.y;
-  } else {
-    qb = CAUSAL ? (nqb - 1 - static_cast<int>(blockIdx.x)) : static_cast<int>(blockIdx.x);
-    h = blockIdx.y;
-    b = blockIdx.z;
-  }
-  const int hkv = h / args.group;
+  // Persistent: CTA c walks work items c, c + gridDim.x, ... of a fixed order.
+  // Non-causal: query blocks of one head adjacent (K/V reuse in L2). Causal:
+  // longest first across all heads (query blocks from the bottom of the mask up,
+  // every head at each step), so the static round-robin stays balanced.
   const int N = args.N;
-  const int q_base = qb * NT * 128;
+  const int nqb = (N + NT * 128 - 1) / (NT * 128);
+  const int HB = args.H * args.B;
+  const int num_items = nqb * HB;
   const int nkv = (N + 127) / 128;
-  int n_t[NT];
-  int n_max = 0;
+  struct Item {
+    int qb, h, b, hkv, q_base, n_max;
+    int n_t[NT];
+  };
+  // k-th work item of this CTA: round-robin; causal rounds alternate direction
+  // (boustrophedon) so the heavier items of each round do not land on the same CTAs
+  auto item_of = [&](int k) {
+    const int G = static_cast<int>(gridDim.x), c = static_cast<int>(blockIdx.x);
+    return k * G + ((CAUSAL && (k & 1)) ? G - 1 - c : c);
+  };
+  auto decode = [&](int lin) {
+    Item w;
+    const int hb = CAUSAL ? lin % HB : lin / nqb;
+    w.qb = CAUSAL ? nqb - 1 - lin / HB : lin % nqb;
+    w.h = hb % args.H;
+    w.b = hb / args.H;
+    w.hkv = w.h / args.group;
+    w.q_base = w.qb * NT * 128;
+    w.n_max = 0;
 #pragma unroll
-  for (int t = 0; t < NT; ++t) {
-    const int r0 = q_base + t * 128;
-    n_t[t] = (r0 < N) ? (CAUSAL ? min(nkv, r0 / 128 + 1) : nkv) : 0;
-    n_max = max(n_max, n_t[t]);
-  }
+    for (int t = 0; t < NT; ++t) {
+      const int r0 = w.q_base + t * 128;
+      w.n_t[t] = (r0 < N) ? (CAUSAL ? min(nkv, r0 / 128 + 1) : nkv) : 0;
+      w.n_max = max(w.n_max, w.n_t[t]);
+    }
+    return w;
+  };
 
   if (warp == T::MMA_WARP) {
     if (ptx::lane_id() == 0) {
@@ -216,6 +222,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
         ptx::mbar_init(&p_full[t], 8);  // one arrival per softmax warp
         ptx::mbar_init(&o_full[t], 1);
       }
+      ptx::mbar_init(q_empty, 1);
       ptx::fence_mbar_init();
     }
     __syncwarp();
@@ -234,31 +241,36 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
   if (warp == T::LOAD_WARP) {
     // ------------------------------------------------------------ producer
     if (ptx::elect_one()) {
-      int nvalid = 0;
+      int item = 0;  // K / V loads so far (the ring position)
+      int itl = 0;   // work items so far
+      for (int lin = item_of(0); lin < num_items; lin = item_of(++itl)) {
+        const Item w = decode(lin);
+        if (itl > 0) ptx::mbar_wait(q_empty, (itl - 1) & 1);
+        int nvalid = 0;
 #pragma unroll
-      for (int t = 0; t < NT; ++t) nvalid += n_t[t] > 0;
-      ptx::mbar_arrive_expect_tx(q_full, nvalid * T::TILE_BYTES);
+        for (int t = 0; t < NT; ++t) nvalid += w.n_t[t] > 0;
+        ptx::mbar_arrive_expect_tx(q_full, nvalid * T::TILE_BYTES);
 #pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        if (n_t[t] == 0) continue;
-#pragma unroll
-        for (int c = 0; c < T::CHUNKS; ++c)
-          ptx::tma_load_4d(smem + T::OFF_Q + t * T::TILE_BYTES + c * T::CHUNK_BYTES, &tmQ,
-                           q_full, c * T::CHUNK_ELEMS, h, q_base + t * 128, b, ptx::kEvictFirst);
-      }
-      int item = 0;
-      for (int j = 0; j < n_max; ++j) {
-#pragma unroll
-        for (int kv = 0; kv < 2; ++kv, ++item) {
-          const int slot = item % T::STAGES;
-          const uint32_t ph = (item / T::STAGES) & 1;
-          ptx::mbar_wait(&kv_empty[slot], ph ^ 1);
-          ptx::mbar_arrive_expect_tx(&kv_full[slot], T::TILE_BYTES);
-          uint8_t* dst = smem + T::OFF_KV + slot * T::TILE_BYTES;
+        for (int t = 0; t < NT; ++t) {
+          if (w.n_t[t] == 0) continue;
 #pragma unroll
           for (int c = 0; c < T::CHUNKS; ++c)
-            ptx::tma_load_4d(dst + c * T::CHUNK_BYTES, kv ? &tmV : &tmK, &kv_full[slot],
-                             c * T::CHUNK_ELEMS, hkv, j * 128, b, ptx::kEvictLast);
+            ptx::tma_load_4d(smem + T::OFF_Q + t * T::TILE_BYTES + c * T::CHUNK_BYTES, &tmQ,
+                             q_full, c * T::CHUNK_ELEMS, w.h, w.q_base + t * 128, w.b, ptx::kEvictFirst);
+        }
+        for (int j = 0; j < w.n_max; ++j) {
+#pragma unroll
+          for (int kv = 0; kv < 2; ++kv, ++item) {
+            const int slot = item % T::STAGES;
+            const uint32_t ph = (item / T::STAGES) & 1;
+            ptx::mbar_wait(&kv_empty[slot], ph ^ 1);
+            ptx::mbar_arrive_expect_tx(&kv_full[slot], T::TILE_BYTES);
+            uint8_t* dst = smem + T::OFF_KV + slot * T::TILE_BYTES;
+#pragma unroll
+            for (int c = 0; c < T::CHUNKS; ++c)
+              ptx::tma_load_4d(dst + c * T::CHUNK_BYTES, kv ? &tmV : &tmK, &kv_full[slot],
+                               c * T::CHUNK_ELEMS, w.hkv, j * 128, w.b, ptx::kEvictLast);
+          }
         }
       }
     }
@@ -296,44 +308,55 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
                             (acc || k > 0) ? 1u : 0u);
         }
       };
-      ptx::mbar_wait(q_full, 0);
-      if (n_max > 0) {
-        ptx::mbar_wait(&kv_full[0], 0);
-        ptx::tc_fence_after();
+      int kvi = 0;  // ring position of this item's K_0
+      int itl = 0;
+      int pc[NT];   // p_full phases consumed per tile
 #pragma unroll
-        for (int t = 0; t < NT; ++t) {
-          if (n_t[t] == 0) continue;
-          issue_qk(t, 0);
-          ptx::mma_commit(&s_full[t]);
-        }
-        ptx::mma_commit(&kv_empty[0]);
-      }
-      for (int j = 0; j < n_max; ++j) {
-        const int item_v = 2 * j + 1, item_k = 2 * j + 2;
-        const int slot_v = item_v % T::STAGES, slot_k = item_k % T::STAGES;
-        ptx::mbar_wait(&kv_full[slot_v], (item_v / T::STAGES) & 1);
-        bool k_ready = false;
-#pragma unroll
-        for (int t = 0; t < NT; ++t) {
-          if (j >= n_t[t]) continue;
-          ptx::mbar_wait(&p_full[t], j & 1);
-          FA3B_TP(t, j, 6);
+      for (int t = 0; t < NT; ++t) pc[t] = 0;
+      for (int lin = item_of(0); lin < num_items; lin = item_of(++itl)) {
+        const Item w = decode(lin);
+        ptx::mbar_wait(q_full, itl & 1);
+        {
+          const int slot0 = kvi % T::STAGES;
+          ptx::mbar_wait(&kv_full[slot0], (kvi / T::STAGES) & 1);
           ptx::tc_fence_after();
-          issue_pv(t, slot_v, j > 0);
-          if (j + 1 < n_t[t]) {
-            if (!k_ready) {
-              ptx::mbar_wait(&kv_full[slot_k], (item_k / T::STAGES) & 1);
-              ptx::tc_fence_after();
-              k_ready = true;
-            }
-            issue_qk(t, slot_k);
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            if (w.n_t[t] == 0) continue;
+            issue_qk(t, slot0);
             ptx::mma_commit(&s_full[t]);
-          } else {
-            ptx::mma_commit(&o_full[t]);
           }
+          ptx::mma_commit(&kv_empty[slot0]);
         }
-        ptx::mma_commit(&kv_empty[slot_v]);
-        if (k_ready) ptx::mma_commit(&kv_empty[slot_k]);
+        for (int j = 0; j < w.n_max; ++j) {
+          const int item_v = kvi + 2 * j + 1, item_k = kvi + 2 * j + 2;
+          const int slot_v = item_v % T::STAGES, slot_k = item_k % T::STAGES;
+          ptx::mbar_wait(&kv_full[slot_v], (item_v / T::STAGES) & 1);
+          bool k_ready = false;
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            if (j >= w.n_t[t]) continue;
+            ptx::mbar_wait(&p_full[t], pc[t]++ & 1);
+            if (itl == 0) FA3B_TP(t, j, 6);
+            ptx::tc_fence_after();
+            issue_pv(t, slot_v, j > 0);
+            if (j + 1 < w.n_t[t]) {
+              if (!k_ready) {
+                ptx::mbar_wait(&kv_full[slot_k], (item_k / T::STAGES) & 1);
+                ptx::tc_fence_after();
+                k_ready = true;
+              }
+              issue_qk(t, slot_k);
+              ptx::mma_commit(&s_full[t]);
+            } else {
+              ptx::mma_commit(&o_full[t]);
+            }
+          }
+          ptx::mma_commit(&kv_empty[slot_v]);
+          if (k_ready) ptx::mma_commit(&kv_empty[slot_k]);
+        }
+        ptx::mma_commit(q_empty);  // fires once every MMA of this item has read Q
+        kvi += 2 * w.n_max;
       }
     }
   } else {
@@ -346,8 +369,13 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
     const uint32_t tO = tmem + lane_base + T::o_col(t);
     float* xch = reinterpret_cast<float*>(smem + T::OFF_XCH) + t * 512;  // [2 buf][2 half][128]
     const uint32_t bar_id = 1 + t;
+    int sc = 0, xc = 0, oc = 0;  // s_full / exchange-buffer / o_full uses so far
+    int itl = 0;
+    for (int lin = item_of(0); lin < num_items; lin = item_of(++itl)) {
+    const Item w = decode(lin);
+    const int b = w.b, h = w.h, hkv = w.hkv, q_base = w.q_base;
     const int q_row = q_base + t * 128 + r;
-    const int nt = (t == 0) ? n_t[0] : n_t[NT - 1];
+    const int nt = (t == 0) ? w.n_t[0] : w.n_t[NT - 1];
     constexpr int HC = 64;               // columns per half
     constexpr int DH = D / 2;            // O columns per half
     float sl2 = args.scale_log2;
@@ -402,12 +430,13 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
           v_cur = vs;
         }
       }
-      const bool tr = (warp & 7) == 0 && ptx::lane_id() == 0;
+      const bool tr = itl == 0 && (warp & 7) == 0 && ptx::lane_id() == 0;
       if (tr) FA3B_TP(t, j, 0);
-      ptx::mbar_wait(&s_full[t], j & 1);
+      ptx::mbar_wait(&s_full[t], sc & 1);
+      ++sc;
       if (tr) FA3B_TP(t, j, 1);
 #ifdef FA3B_TRACE
-      if (j == 0 && threadIdx.x == 0) FA3B_CTA(3, fa3b_gtime());
+      if (itl == 0 && j == 0 && threadIdx.x == 0) FA3B_CTA(3, fa3b_gtime());
 #endif
       ptx::tc_fence_after();
       float s[HC];
@@ -440,7 +469,8 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       a0 = ptx::max3(a0, s[60], s[61]);
       a1 = ptx::max3(a1, s[62], s[63]);
       const float pm = fmaxf(ptx::max3(a0, a1, a2), a3);
-      float* xb = xch + (j & 1) * 256;
+      float* xb = xch + (xc & 1) * 256;
+      ++xc;
       ptx::sts_f32(xb + hh * 128 + r, pm);
       // P = 2^(s * slj - msub) for this half: FFMA2 pairs; EMU of every 8 pairs go
       // through the FMA-pipe polynomial, the rest through MUFU.EX2; FADD2 sums.
@@ -517,11 +547,13 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
     }
     if (nt > 0) {
       // ---------------------------------------------------------- epilogue
-      float* xb = xch + (nt & 1) * 256;
+      float* xb = xch + (xc & 1) * 256;
+      ++xc;
       ptx::sts_f32(xb + hh * 128 + r, l);
       ptx::named_bar_sync(bar_id, 256);
       l += ptx::lds_f32(xb + (hh ^ 1) * 128 + r);
-      ptx::mbar_wait(&o_full[t], 0);
+      ptx::mbar_wait(&o_full[t], oc & 1);
+      ++oc;
       ptx::tc_fence_after();
       if constexpr (FP8) out_scale = v_cur * ptx::ex2(thr) * (1.f / 448.f);
       const float inv = l > 0.f ? out_scale / l : 0.f;
@@ -562,6 +594,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
         args.lse[(static_cast<size_t>(b) * args.H + h) * N + q_row] = lse;
       }
     }
+    }  // work items
   }
 
   ptx::tc_fence_before();
