@@ -245,20 +245,26 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       int itl = 0;   // work items so far
       for (int lin = item_of(0); lin < num_items; lin = item_of(++itl)) {
         const Item w = decode(lin);
-        if (itl > 0) ptx::mbar_wait(q_empty, (itl - 1) & 1);
-        int nvalid = 0;
+        auto load_q = [&]() {
+          if (itl > 0) ptx::mbar_wait(q_empty, (itl - 1) & 1);
+          int nvalid = 0;
 #pragma unroll
-        for (int t = 0; t < NT; ++t) nvalid += w.n_t[t] > 0;
-        ptx::mbar_arrive_expect_tx(q_full, nvalid * T::TILE_BYTES);
+          for (int t = 0; t < NT; ++t) nvalid += w.n_t[t] > 0;
+          ptx::mbar_arrive_expect_tx(q_full, nvalid * T::TILE_BYTES);
 #pragma unroll
-        for (int t = 0; t < NT; ++t) {
-          if (w.n_t[t] == 0) continue;
+          for (int t = 0; t < NT; ++t) {
+            if (w.n_t[t] == 0) continue;
 #pragma unroll
-          for (int c = 0; c < T::CHUNKS; ++c)
-            ptx::tma_load_4d(smem + T::OFF_Q + t * T::TILE_BYTES + c * T::CHUNK_BYTES, &tmQ,
-                             q_full, c * T::CHUNK_ELEMS, w.h, w.q_base + t * 128, w.b, ptx::kEvictFirst);
-        }
+            for (int c = 0; c < T::CHUNKS; ++c)
+              ptx::tma_load_4d(smem + T::OFF_Q + t * T::TILE_BYTES + c * T::CHUNK_BYTES, &tmQ,
+                               q_full, c * T::CHUNK_ELEMS, w.h, w.q_base + t * 128, w.b,
+                               ptx::kEvictFirst);
+          }
+        };
+        // this item's first K/V block streams into the ring while the previous
+        // item's last GEMMs still hold the Q buffer
         for (int j = 0; j < w.n_max; ++j) {
+          if (j == 1) load_q();
 #pragma unroll
           for (int kv = 0; kv < 2; ++kv, ++item) {
             const int slot = item % T::STAGES;
@@ -272,6 +278,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
                                c * T::CHUNK_ELEMS, w.hkv, j * 128, w.b, ptx::kEvictLast);
           }
         }
+        if (w.n_max == 1) load_q();
       }
     }
   } else if (warp == T::MMA_WARP) {
