@@ -175,8 +175,8 @@ struct BwdTraits {
   static constexpr int OFF_VEC = OFF_STG + 2 * CHUNK_BYTES;     // LSE2[2][128], Delta[2][128]
   static constexpr int OFF_BAR = OFF_VEC + 4 * 512;
   // kv_full, ring_full[RING], ring_empty[RING], vec_full[2], vec_empty[2], s_full,
-  // dp_full, pa_full, pb_full, dq_full, dq_free, dkv_full
-  static constexpr int NUM_BARS = 12 + 2 * RING;
+  // dp_full, pa_full, pb_full, dq_full, dq_free, dkv_full, kv_empty
+  static constexpr int NUM_BARS = 13 + 2 * RING;
   static constexpr int SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr int COL_S = 0, COL_DP = 128, COL_DV = 256, COL_DK = 256 + D;
   static constexpr int COL_DQ = DQ_IN_DP ? COL_DP : 256 + 2 * D;
@@ -217,32 +217,37 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
   uint64_t* dq_full = s_full + 4;
   uint64_t* dq_free = s_full + 5;
   uint64_t* dkv_full = s_full + 6;
+  uint64_t* kv_empty = s_full + 7;  // this item's K and V tiles are consumed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + T::NUM_BARS);
   float* lse_s = reinterpret_cast<float*>(smem + T::OFF_VEC);  // [2][128]
   float* del_s = lse_s + 256;                                   // [2][128]
 
   const int warp = static_cast<int>(ptx::warp_id());
-#ifndef FA3B_CAUSAL_LPT
-#define FA3B_CAUSAL_LPT 1
-#endif
-  // causal: KV tile j sees nq - j query tiles; launch longest-first across all heads
-  int j, hkv, b;
-  if (CAUSAL && FA3B_CAUSAL_LPT) {
-    const int lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-    const int hb = gridDim.y * gridDim.z;
-    j = lin / hb;
-    hkv = (lin % hb) % gridDim.y;
-    b = (lin % hb) / gridDim.y;
-  } else {
-    j = blockIdx.x;  // KV tile
-    hkv = blockIdx.y;
-    b = blockIdx.z;
-  }
+  // Persistent: CTA c walks work items (KV tile j, KV head, batch) c, c + G, ...
+  // Causal KV tile j sees nq - j query tiles: items go longest-first across all
+  // heads, in boustrophedon rounds so each round's heavy items spread over CTAs.
   const int N = args.N;
   const int nq = args.Npad / 128;
-  const int i0 = CAUSAL ? j : 0;
-  const int per_head = nq - i0;
-  const int n_iter = per_head * args.group;
+  const int HB = args.Hkv * args.B;
+  const int num_items = nq * HB;
+  auto item_of = [&](int k) {
+    const int G = static_cast<int>(gridDim.x), c = static_cast<int>(blockIdx.x);
+    return k * G + ((CAUSAL && (k & 1)) ? G - 1 - c : c);
+  };
+  struct Item {
+    int j, hkv, b, i0, per_head, n_iter;
+  };
+  auto decode = [&](int lin) {
+    Item w;
+    const int hb = CAUSAL ? lin % HB : lin / nq;
+    w.j = CAUSAL ? lin / HB : lin % nq;
+    w.hkv = hb % args.Hkv;
+    w.b = hb / args.Hkv;
+    w.i0 = CAUSAL ? w.j : 0;
+    w.per_head = nq - w.i0;
+    w.n_iter = w.per_head * args.group;
+    return w;
+  };
   // ring slot and parity of tile t (t = 2i for Q_i, 2i + 1 for dO_i)
   auto slot_of = [](int t) { return t % T::RING; };
   auto par_of = [](int t) { return static_cast<uint32_t>((t / T::RING) & 1); };
@@ -267,6 +272,7 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
       ptx::mbar_init(dq_full, 1);
       ptx::mbar_init(dq_free, 4);  // one arrival per dQ-writer warp
       ptx::mbar_init(dkv_full, 1);
+      ptx::mbar_init(kv_empty, 1);
       ptx::fence_mbar_init();
     }
     __syncwarp();
@@ -287,37 +293,44 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
         ptx::prefetch_tmap(&tmK);
         ptx::prefetch_tmap(&tmV);
         ptx::prefetch_tmap(&tmdO);
-        ptx::mbar_arrive_expect_tx(kv_full, 2 * T::TILE_BYTES);
-        for (int c = 0; c < D / 64; ++c) {
-          ptx::tma_load_4d(smem + T::OFF_K + c * T::CHUNK_BYTES, &tmK, kv_full, c * 64, hkv, j * 128, b,
-                           ptx::kEvictFirst);
-          ptx::tma_load_4d(smem + T::OFF_V + c * T::CHUNK_BYTES, &tmV, kv_full, c * 64, hkv, j * 128, b,
-                           ptx::kEvictFirst);
-        }
-        for (int it = 0; it < n_iter; ++it) {
-          const int h = hkv * args.group + it / per_head;
-          const int i = i0 + it % per_head;
-          const size_t vec = (static_cast<size_t>(b) * args.H + h) * args.Npad + i * 128;
+        int gi = 0;  // Q tiles (iterations) over all items: ring and vector positions
+        int itl = 0;
+        for (int lin = item_of(0); lin < num_items; lin = item_of(++itl)) {
+          const Item w = decode(lin);
+          if (itl > 0) ptx::mbar_wait(kv_empty, (itl - 1) & 1);
+          ptx::mbar_arrive_expect_tx(kv_full, 2 * T::TILE_BYTES);
+          for (int c = 0; c < D / 64; ++c) {
+            ptx::tma_load_4d(smem + T::OFF_K + c * T::CHUNK_BYTES, &tmK, kv_full, c * 64, w.hkv, w.j * 128,
+                             w.b, ptx::kEvictFirst);
+            ptx::tma_load_4d(smem + T::OFF_V + c * T::CHUNK_BYTES, &tmV, kv_full, c * 64, w.hkv, w.j * 128,
+                             w.b, ptx::kEvictFirst);
+          }
+          for (int it = 0; it < w.n_iter; ++it, ++gi) {
+            const int h = w.hkv * args.group + it / w.per_head;
+            const int i = w.i0 + it % w.per_head;
+            const size_t vec = (static_cast<size_t>(w.b) * args.H + h) * args.Npad + i * 128;
 #pragma unroll
-          for (int which = 0; which < 2; ++which) {  // Q_i then dO_i
-            const int t = 2 * it + which;
-            const int s = slot_of(t);
-            ptx::mbar_wait(&ring_empty[s], par_of(t) ^ 1);
-            const bool vec_here = which == 0 && !T::VEC_OWN;
-            ptx::mbar_arrive_expect_tx(&ring_full[s], T::TILE_BYTES + (vec_here ? 1024 : 0));
-            for (int c = 0; c < D / 64; ++c)
-              ptx::tma_load_4d(smem + T::OFF_RING + s * T::TILE_BYTES + c * T::CHUNK_BYTES,
-                               which ? &tmdO : &tmQ, &ring_full[s], c * 64, h, i * 128, b, ptx::kEvictLast);
-            if (which == 0) {
-              const int vs = it & 1;
-              uint64_t* vbar = &ring_full[s];
-              if (T::VEC_OWN) {
-                ptx::mbar_wait(&vec_empty[vs], ((it >> 1) & 1) ^ 1);
-                ptx::mbar_arrive_expect_tx(&vec_full[vs], 1024);
-                vbar = &vec_full[vs];
+            for (int which = 0; which < 2; ++which) {  // Q_i then dO_i
+              const int t = 2 * gi + which;
+              const int s = slot_of(t);
+              ptx::mbar_wait(&ring_empty[s], par_of(t) ^ 1);
+              const bool vec_here = which == 0 && !T::VEC_OWN;
+              ptx::mbar_arrive_expect_tx(&ring_full[s], T::TILE_BYTES + (vec_here ? 1024 : 0));
+              for (int c = 0; c < D / 64; ++c)
+                ptx::tma_load_4d(smem + T::OFF_RING + s * T::TILE_BYTES + c * T::CHUNK_BYTES,
+                                 which ? &tmdO : &tmQ, &ring_full[s], c * 64, h, i * 128, w.b,
+                                 ptx::kEvictLast);
+              if (which == 0) {
+                const int vs = gi & 1;
+                uint64_t* vbar = &ring_full[s];
+                if (T::VEC_OWN) {
+                  ptx::mbar_wait(&vec_empty[vs], ((gi >> 1) & 1) ^ 1);
+                  ptx::mbar_arrive_expect_tx(&vec_full[vs], 1024);
+                  vbar = &vec_full[vs];
+                }
+                ptx::bulk_load(lse_s + vs * 128, args.lse2 + vec, 512, vbar);
+                ptx::bulk_load(del_s + vs * 128, args.delta + vec, 512, vbar);
               }
-              ptx::bulk_load(lse_s + vs * 128, args.lse2 + vec, 512, vbar);
-              ptx::bulk_load(del_s + vs * 128, args.delta + vec, 512, vbar);
             }
           }
         }
@@ -352,80 +365,91 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
                             ptx::sw128_desc(do_addr + off, 16, 1024), idesc_dp, k > 0);
           }
         };
-        ptx::mbar_wait(kv_full, 0);
-        wait_tile(0);
-        issue_s(0);
-        ptx::mma_commit(s_full);
-        wait_tile(1);
-        issue_dp(0);
-        ptx::mma_commit(dp_full);
-        for (int it = 0; it < n_iter; ++it) {
-          const bool more = it + 1 < n_iter;
-          // dV += P^T dO (A = P^T pairs in TMEM, B = dO MN-major); then dO_i is free
-          ptx::mbar_wait(pa_full, it & 1);
-          BWD_TP(it, 0);
-          ptx::tc_fence_after();
-          const uint32_t do_addr = tile_addr(2 * it + 1);
-#pragma unroll
-          for (int t = 0; t < 8; ++t)
-            ptx::mma_f16_ts(tmem + T::COL_DV, tmem + T::COL_S + pair_col(t),
-                            ptx::sw128_desc(do_addr + t * 16 * 128, T::CHUNK_BYTES, 1024), idesc_acc,
-                            (it > 0 || t > 0));
-          if (T::VEC_OWN) ptx::mma_commit(&ring_empty[slot_of(2 * it + 1)]);  // dO_i free early
-#if FA3B_BWD_S_EARLY
-          // S_{i+1} may overwrite the S^T columns as soon as dV_i (the last reader of
-          // P_i^T) is issued: phase A of tile i+1 then overlaps phase B of tile i
-          if (more) {
-            wait_tile(2 * it + 2);
-            issue_s(it + 1);
-            ptx::mma_commit(s_full);
+        int gi = 0;  // global iteration (Q tile) index: ring tiles and barrier phases
+        int itl = 0;
+        for (int lin = item_of(0); lin < num_items; lin = item_of(++itl)) {
+          const Item w = decode(lin);
+          ptx::mbar_wait(kv_full, itl & 1);
+          if (T::DQ_IN_DP && gi > 0) {  // the previous item's last dQ still sits in the dP^T columns
+            ptx::mbar_wait(dq_free, (gi - 1) & 1);
           }
-#endif
-          // dK += dS^T Q (A = dS^T pairs in TMEM, B = Q MN-major); then Q_i, LSE2_i, D_i are free
-          ptx::mbar_wait(pb_full, it & 1);
-          BWD_TP(it, 1);
-          ptx::tc_fence_after();
-          const uint32_t q_addr = tile_addr(2 * it);
-#pragma unroll
-          for (int t = 0; t < 8; ++t)
-            ptx::mma_f16_ts(tmem + T::COL_DK, tmem + T::COL_DP + pair_col(t),
-                            ptx::sw128_desc(q_addr + t * 16 * 128, T::CHUNK_BYTES, 1024), idesc_acc,
-                            (it > 0 || t > 0));
-          ptx::mma_commit(&ring_empty[slot_of(2 * it)]);
-          if (T::VEC_OWN)
-            ptx::mma_commit(&vec_empty[it & 1]);
-          else
-            ptx::mma_commit(&ring_empty[slot_of(2 * it + 1)]);
-#if !FA3B_BWD_S_EARLY
-          if (more) {
-            wait_tile(2 * it + 2);
-            issue_s(it + 1);
-            ptx::mma_commit(s_full);
-          }
-#endif
-          if (!T::DQ_IN_DP && it > 0) {  // own columns: the previous dQ must have been read out
-            ptx::mbar_wait(dq_free, (it - 1) & 1);
+          wait_tile(2 * gi);
+          issue_s(gi);
+          ptx::mma_commit(s_full);
+          wait_tile(2 * gi + 1);
+          issue_dp(gi);
+          ptx::mma_commit(dp_full);
+          for (int it = 0; it < w.n_iter; ++it) {
+            const int g = gi + it;  // global iteration
+            const bool more = it + 1 < w.n_iter;
+            // dV += P^T dO (A = P^T pairs in TMEM, B = dO MN-major); then dO_i is free
+            ptx::mbar_wait(pa_full, g & 1);
+            if (itl == 0) BWD_TP(it, 0);
             ptx::tc_fence_after();
-          }
+            const uint32_t do_addr = tile_addr(2 * g + 1);
 #pragma unroll
-          for (int t = 0; t < 8; ++t) {  // dQ = dS K: 16 KV rows per step, both operands MN-major
-            const uint32_t off = t * 16 * 128;
-            ptx::mma_f16_ss(tmem + T::COL_DQ, ptx::sw128_desc(ds_addr + off, T::CHUNK_BYTES, 1024),
-                            ptx::sw128_desc(k_addr + off, T::CHUNK_BYTES, 1024), idesc_dq, t > 0);
-          }
-          ptx::mma_commit(dq_full);
-          if (more) {
-            if (T::DQ_IN_DP) {  // dP_{i+1} overwrites the dQ_i columns once they are read out
-              ptx::mbar_wait(dq_free, it & 1);
+            for (int t = 0; t < 8; ++t)
+              ptx::mma_f16_ts(tmem + T::COL_DV, tmem + T::COL_S + pair_col(t),
+                              ptx::sw128_desc(do_addr + t * 16 * 128, T::CHUNK_BYTES, 1024), idesc_acc,
+                              (it > 0 || t > 0));
+            if (T::VEC_OWN) ptx::mma_commit(&ring_empty[slot_of(2 * g + 1)]);  // dO_i free early
+#if FA3B_BWD_S_EARLY
+            // S_{i+1} may overwrite the S^T columns as soon as dV_i (the last reader of
+            // P_i^T) is issued: phase A of tile i+1 then overlaps phase B of tile i
+            if (more) {
+              wait_tile(2 * g + 2);
+              issue_s(g + 1);
+              ptx::mma_commit(s_full);
+            }
+#endif
+            // dK += dS^T Q (A = dS^T pairs in TMEM, B = Q MN-major); then Q_i, LSE2_i, D_i are free
+            ptx::mbar_wait(pb_full, g & 1);
+            if (itl == 0) BWD_TP(it, 1);
+            ptx::tc_fence_after();
+            const uint32_t q_addr = tile_addr(2 * g);
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+              ptx::mma_f16_ts(tmem + T::COL_DK, tmem + T::COL_DP + pair_col(t),
+                              ptx::sw128_desc(q_addr + t * 16 * 128, T::CHUNK_BYTES, 1024), idesc_acc,
+                              (it > 0 || t > 0));
+            ptx::mma_commit(&ring_empty[slot_of(2 * g)]);
+            if (T::VEC_OWN)
+              ptx::mma_commit(&vec_empty[g & 1]);
+            else
+              ptx::mma_commit(&ring_empty[slot_of(2 * g + 1)]);
+#if !FA3B_BWD_S_EARLY
+            if (more) {
+              wait_tile(2 * g + 2);
+              issue_s(g + 1);
+              ptx::mma_commit(s_full);
+            }
+#endif
+            if (!T::DQ_IN_DP && g > 0) {  // own columns: the previous dQ must have been read out
+              ptx::mbar_wait(dq_free, (g - 1) & 1);
               ptx::tc_fence_after();
             }
-            BWD_TP(it, 2);
-            wait_tile(2 * it + 3);
-            issue_dp(it + 1);
-            ptx::mma_commit(dp_full);
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {  // dQ = dS K: 16 KV rows per step, both operands MN-major
+              const uint32_t off = t * 16 * 128;
+              ptx::mma_f16_ss(tmem + T::COL_DQ, ptx::sw128_desc(ds_addr + off, T::CHUNK_BYTES, 1024),
+                              ptx::sw128_desc(k_addr + off, T::CHUNK_BYTES, 1024), idesc_dq, t > 0);
+            }
+            ptx::mma_commit(dq_full);
+            if (more) {
+              if (T::DQ_IN_DP) {  // dP_{i+1} overwrites the dQ_i columns once they are read out
+                ptx::mbar_wait(dq_free, g & 1);
+                ptx::tc_fence_after();
+              }
+              if (itl == 0) BWD_TP(it, 2);
+              wait_tile(2 * g + 3);
+              issue_dp(g + 1);
+              ptx::mma_commit(dp_full);
+            }
           }
+          ptx::mma_commit(dkv_full);
+          ptx::mma_commit(kv_empty);  // K and V of this item are no longer read
+          gi += w.n_iter;
         }
-        ptx::mma_commit(dkv_full);
       }
     }
   } else if (warp >= T::DRAIN_WARP0) {
@@ -437,11 +461,15 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
     const bool leader = dw == 0 && lane == 0;
     const int r = 32 * dw + lane;  // query row of the tile = TMEM lane
     constexpr int NB = D / 32;     // 128 x 32 fp32 boxes per dQ tile
-    for (int it = 0; it < n_iter; ++it) {
-      const int h = hkv * args.group + it / per_head;
-      const int i = i0 + it % per_head;
-      ptx::mbar_wait(dq_full, it & 1);
-      if (dw == 0 && lane == 0) BWD_TP(it, 12);
+    int gi = 0, itl = 0;
+    for (int lin = item_of(0); lin < num_items; lin = item_of(++itl)) {
+    const Item w = decode(lin);
+    const int b = w.b;
+    for (int it = 0; it < w.n_iter; ++it, ++gi) {
+      const int h = w.hkv * args.group + it / w.per_head;
+      const int i = w.i0 + it % w.per_head;
+      ptx::mbar_wait(dq_full, gi & 1);
+      if (itl == 0 && dw == 0 && lane == 0) BWD_TP(it, 12);
       ptx::tc_fence_after();
       uint32_t v[NB][32];
 #pragma unroll
@@ -450,13 +478,13 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(dq_free);
-      if (dw == 0 && lane == 0) BWD_TP(it, 13);
+      if (itl == 0 && dw == 0 && lane == 0) BWD_TP(it, 13);
       if constexpr (D == 128) {
         // four boxes through two staging buffers: each buffer is refilled once the
         // reduce-add issued two boxes earlier has finished reading it
 #pragma unroll
         for (int c = 0; c < NB; ++c) {
-          if (leader && (it > 0 || c >= 2)) ptx::bulk_wait_group_read<1>();
+          if (leader && (gi > 0 || c >= 2)) ptx::bulk_wait_group_read<1>();
           ptx::named_bar_sync(3, 128);
           uint8_t* stg = smem + T::OFF_STG + (c & 1) * T::CHUNK_BYTES + r * 128;
 #pragma unroll
@@ -492,29 +520,34 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
         }
       }
     }
+    }  // work items
     if (leader) ptx::bulk_wait_group<0>();
   } else {
     // ------------------------------------------------ 2 gradient warpgroups
     const int w = warp >> 2;          // which 64-column half of the query tile
     const int r = threadIdx.x & 127;  // KV row in the tile == TMEM lane
     const uint32_t lane_base = static_cast<uint32_t>(32 * (warp & 3)) << 16;
-    const int kv_row = j * 128 + r;
     const float sl2 = args.scale_log2;
     uint8_t* ds_row = smem + T::OFF_DS + w * T::CHUNK_BYTES + r * 128;
-    for (int it = 0; it < n_iter; ++it) {
-      const int s = it & 1;
-      const int i = i0 + it % per_head;
+    int gi = 0, itl = 0;
+    for (int lin = item_of(0); lin < num_items; lin = item_of(++itl)) {
+    const Item wk = decode(lin);
+    const int j = wk.j, b = wk.b, hkv = wk.hkv;
+    const int kv_row = j * 128 + r;
+    for (int it = 0; it < wk.n_iter; ++it, ++gi) {
+      const int s = gi & 1;
+      const int i = wk.i0 + it % wk.per_head;
       const float* lse_v = lse_s + s * 128 + 64 * w;
       const float* del_v = del_s + s * 128 + 64 * w;
       // phase A: P^T = exp2(S^T |alpha| log2e - LSE2) -> TMEM pairs, feeds dV
-      const bool trc = (warp & 3) == 0 && ptx::lane_id() == 0;
-      ptx::mbar_wait(s_full, it & 1);
+      const bool trc = itl == 0 && (warp & 3) == 0 && ptx::lane_id() == 0;
+      ptx::mbar_wait(s_full, gi & 1);
       if (trc) BWD_TP(it, 4 + 4 * w);
       ptx::tc_fence_after();
       uint32_t sr[64];
       ptx::tmem_ld32(tmem + lane_base + T::COL_S + 64 * w, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
       ptx::tmem_ld32(tmem + lane_base + T::COL_S + 64 * w + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
-      if (T::VEC_OWN) ptx::mbar_wait(&vec_full[s], (it >> 1) & 1);
+      if (T::VEC_OWN) ptx::mbar_wait(&vec_full[s], (gi >> 1) & 1);
       ptx::tmem_wait_ld();
       const bool diag = CAUSAL && i == j;
       const int lim = kv_row - (i * 128 + 64 * w);  // causal: query column c is visible iff c >= lim
@@ -553,7 +586,7 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
       if (trc) BWD_TP(it, 5 + 4 * w);
       // phase B: dS^T = P^T o (dP^T - D) -> TMEM pairs (feeds dK) and the swizzled
       // shared tile (feeds dQ), in two 32-column halves
-      ptx::mbar_wait(dp_full, it & 1);
+      ptx::mbar_wait(dp_full, gi & 1);
       if (trc) BWD_TP(it, 6 + 4 * w);
       ptx::tc_fence_after();
 #pragma unroll
@@ -593,7 +626,7 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
       if (trc) BWD_TP(it, 7 + 4 * w);
     }
     // ------------------------------------------------ epilogue: dK, dV
-    ptx::mbar_wait(dkv_full, 0);
+    ptx::mbar_wait(dkv_full, itl & 1);
     ptx::tc_fence_after();
     const bool row_ok = kv_row < N;
 #pragma unroll
@@ -620,6 +653,7 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
         for (int e = 0; e < 4; ++e) dst[e] = make_uint4(pk2[4 * e], pk2[4 * e + 1], pk2[4 * e + 2], pk2[4 * e + 3]);
       }
     }
+    }  // work items
   }
 
   ptx::tc_fence_before();
@@ -692,7 +726,9 @@ int launch_bwd_main(const fa3b_bwd_params& p, const Workspace& ws, int Npad, cud
   const uint32_t idesc_acc = ptx::make_idesc(128, D, fmt, fmt, false, true, false);
   // dQ = dS K (M = 128 query rows, N = D), both operands MN-major
   const uint32_t idesc_dq = ptx::make_idesc(128, D, fmt, fmt, true, true, false);
-  dim3 grid(Npad / 128, p.heads_kv, p.batch);
+  // persistent: one CTA per SM over (KV tile, KV head, batch) work items
+  const long long items = static_cast<long long>(Npad / 128) * p.heads_kv * p.batch;
+  const int grid = static_cast<int>(items < num_sms() ? items : num_sms());
   kern<<<grid, Tr::NUM_THREADS, Tr::SMEM_BYTES, st>>>(tq, tk, tv, tdo, tdq, a, idesc_s, idesc_dp, idesc_acc,
                                                       idesc_dq);
   cudaError_t e = cudaGetLastError();
