@@ -141,8 +141,8 @@ struct BwdArgs {
 // reduce-adds (cp.reduce.async.bulk.tensor ... .add), the paper's dQ-writer role
 // without per-element atomics on the load/store pipe.
 //
-// Q_i and dO_i share a ring of tile slots (tile 2i = Q_i, 2i+1 = dO_i; 3 slots at
-// d = 128, 4 at d = 64):
+// Q_i and dO_i live in tile slots (tile 2i = Q_i, 2i+1 = dO_i): Q double-buffered,
+// dO single-buffered at d = 128 (3 slots) or double-buffered at d = 64 (4 slots):
 // dO_i is released after dV_i, Q_i after dK_i, which leaves room at d = 128 for
 // the dQ staging boxes. LSE2_i and D_i arrive by cp.async.bulk into their own
 // double buffer.
@@ -249,8 +249,17 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
     return w;
   };
   // ring slot and parity of tile t (t = 2i for Q_i, 2i + 1 for dO_i)
-  auto slot_of = [](int t) { return t % T::RING; };
-  auto par_of = [](int t) { return static_cast<uint32_t>((t / T::RING) & 1); };
+  // Fixed slots: Q_i alternates between slots 0 and 1; dO_i takes slot 2 (3-slot ring,
+  // d = 128: dO_{i+1} reloads as soon as dV_i has read dO_i, a full GEMM chain before
+  // dP_{i+1} needs it) or alternates between 2 and 3 (4 slots, d = 64).
+  auto slot_of = [](int t) {
+    const int i = t >> 1;
+    return (t & 1) ? (T::RING == 3 ? 2 : 2 + (i & 1)) : (i & 1);
+  };
+  auto par_of = [](int t) {
+    const int i = t >> 1;
+    return static_cast<uint32_t>(((t & 1) && T::RING == 3) ? (i & 1) : ((i >> 1) & 1));
+  };
 
   if (warp == T::MMA_WARP) {
     // the tile offsets above assume a 1024-byte aligned dynamic smem base
