@@ -7,20 +7,19 @@
 // scale = amax / 448 (1 if amax == 0), code = round_to(x * (1 / scale), e4m3)
 // (core/src/formats.cpp:45-61, RNE, saturating).
 //
-// The arithmetic is FP64 with the reference's butterfly and rounding order, so
+// The arithmetic is FP64 with the reference's rounding points (the butterfly
+// sums of 16-bit or fp32 inputs are exact in FP64, so their order is free), so
 // codes and scales are byte-identical to the reference for the same input
-// values (tests/test_fp8_gpu.py). The kernel is HBM-bound (2-4 bytes read,
-// 1 byte written per element); FP64 costs ~7 flop/element, well under the
-// B200 FP64 rate needed to stay memory-bound.
+// values (tests/test_fp8_gpu.py). Algorithmic traffic: 2-4 bytes read and 1
+// byte written per element.
 //
-// Layout: one CTA per (row block, head, batch); one warp per row, lane l
-// holds the E = d/32 contiguous elements [l E, l E + E). Butterfly stages with
-// len < E stay in the thread, larger ones exchange with lane l ^ (len / E)
-// through shuffles. Each lane's E source elements arrive in one or two vector
-// loads, all rows of a warp in flight together. 128-row blocks at d <= 128 keep
-// the whole transformed block in registers (16 warps x 8 rows) across the amax
-// reduction; d = 256 and other block sizes (per tensor) take two passes that
-// recompute the transform (the second read hits L2).
+// Layout (see Quad): 4 lanes per row at d <= 128 (8 at d = 256), each holding
+// d / 4 (d / 8) contiguous elements, so all but the last two (three) butterfly
+// stages run in registers; vector loads and stores. 128-row blocks at
+// d <= 128 keep the whole transformed block in registers across the amax
+// (one read of the input); d = 256 and other block sizes (per tensor) take two
+// passes that recompute the transform (the second read hits L2), split over an
+// 8-CTA cluster when there are too few blocks to fill the GPU.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -59,37 +58,6 @@ __device__ __forceinline__ uint8_t e4m3_code(double x, bool saturate) {
   return sign | static_cast<uint8_t>(code);
 }
 
-template <int E>
-__device__ __forceinline__ void fwht_warp(double (&v)[E], int lane) {
-  constexpr int D = 32 * E;
-#pragma unroll
-  for (int len = 1; len < D; len <<= 1) {
-    if (len < E) {
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        if ((e & len) == 0) {
-          const double a = v[e], b = v[e + len];
-          v[e] = a + b;
-          v[e + len] = a - b;
-        }
-      }
-    } else {
-      const int lmask = len / E;
-      // lower lane: v + other; upper lane: other - v; one exact-product DFMA either way
-      // (IEEE addition commutes, so the rounding equals the reference's a + b / a - b)
-      const double sgn = (lane & lmask) ? -1.0 : 1.0;
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const double other = __shfl_xor_sync(0xffffffffu, v[e], lmask);
-        v[e] = fma(sgn, v[e], other);
-      }
-    }
-  }
-  const double norm = 1.0 / sqrt(static_cast<double>(D));
-#pragma unroll
-  for (int e = 0; e < E; ++e) v[e] *= norm;
-}
-
 struct PrepArgs {
   const void* src;
   long long s_sb, s_ss, s_sh;
@@ -100,112 +68,6 @@ struct PrepArgs {
   int N, H, block_rows, nblk, hadamard, saturate;
   unsigned long long signs[4];  // bit i set -> sign_i = +1
 };
-
-// The E contiguous source elements of one lane as raw words: E x 16-bit (4-16 B)
-// or E x fp32 (8-32 B), one or two vector loads.
-template <int E>
-struct RawRow {
-  uint4 w[E / 2 > 2 ? E / 2 : 2];
-};
-
-template <int E>
-__device__ __forceinline__ void load_raw(const PrepArgs& a, int b, int h, int row, int lane,
-                                         RawRow<E>& r) {
-  const size_t base = b * a.s_sb + static_cast<size_t>(row) * a.s_ss + h * a.s_sh + lane * E;
-  if (a.src_dtype == FA3B_DTYPE_F32) {
-    const float* p = static_cast<const float*>(a.src) + base;
-    if constexpr (E == 2) {
-      const uint2 t = __ldg(reinterpret_cast<const uint2*>(p));
-      r.w[0] = make_uint4(t.x, t.y, 0, 0);
-    } else {
-#pragma unroll
-      for (int i = 0; i < E / 4; ++i) r.w[i] = __ldg(reinterpret_cast<const uint4*>(p) + i);
-    }
-  } else {
-    const uint16_t* p = static_cast<const uint16_t*>(a.src) + base;
-    if constexpr (E == 2) {
-      r.w[0].x = __ldg(reinterpret_cast<const unsigned int*>(p));
-    } else if constexpr (E == 4) {
-      const uint2 t = __ldg(reinterpret_cast<const uint2*>(p));
-      r.w[0] = make_uint4(t.x, t.y, 0, 0);
-    } else {
-      r.w[0] = __ldg(reinterpret_cast<const uint4*>(p));
-    }
-  }
-}
-
-template <int E>
-__device__ __forceinline__ void unpack_raw(const PrepArgs& a, const RawRow<E>& r, double (&v)[E]) {
-  const uint32_t* u = reinterpret_cast<const uint32_t*>(&r.w[0]);
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    if (a.src_dtype == FA3B_DTYPE_F32) {
-      v[e] = __uint_as_float(u[e]);
-    } else {
-      const uint16_t bits = static_cast<uint16_t>(u[e >> 1] >> (16 * (e & 1)));
-      v[e] = a.src_dtype == FA3B_DTYPE_BF16 ? __uint_as_float(static_cast<uint32_t>(bits) << 16)
-                                            : __half2float(__ushort_as_half(bits));
-    }
-  }
-}
-
-template <int E>
-__device__ __forceinline__ void transform_row(const PrepArgs& a, int lane, double (&v)[E]) {
-  if (a.hadamard) {
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int i = lane * E + e;
-      if (!((a.signs[i >> 6] >> (i & 63)) & 1ull)) v[e] = -v[e];
-    }
-    fwht_warp<E>(v, lane);
-  }
-}
-
-template <int E>
-__device__ __forceinline__ void load_row(const PrepArgs& a, int b, int h, int row, int lane,
-                                         double (&v)[E]) {
-  RawRow<E> r;
-  load_raw<E>(a, b, h, row, lane, r);
-  unpack_raw<E>(a, r, v);
-  transform_row<E>(a, lane, v);
-}
-
-template <int E>
-__device__ __forceinline__ void store_codes(const PrepArgs& a, int b, int h, int row, int lane,
-                                            const double (&v)[E], double inv) {
-  uint8_t c[E];
-  if (a.saturate) {
-    // FP64 -> FP32 with round-to-odd (truncate, then set the last bit if inexact),
-    // then the hardware RNE saturating e4m3 conversion: rounding to odd at 24
-    // bits before rounding to 4 bits equals rounding the FP64 value directly.
-#pragma unroll
-    for (int e = 0; e < E; e += 2) {
-      float f[2];
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const double t = v[e + u] * inv;
-        float z = __double2float_rz(t);
-        if (static_cast<double>(z) != t) z = __uint_as_float(__float_as_uint(z) | 1u);
-        f[u] = z;
-      }
-      uint16_t pr;
-      asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(pr) : "f"(f[1]), "f"(f[0]));
-      c[e] = static_cast<uint8_t>(pr & 0xFF);
-      c[e + 1] = static_cast<uint8_t>(pr >> 8);
-    }
-  } else {
-#pragma unroll
-    for (int e = 0; e < E; ++e) c[e] = e4m3_code(v[e] * inv, false);
-  }
-  uint8_t* dst = a.dst + b * a.d_sb + static_cast<size_t>(row) * a.d_ss + h * a.d_sh + lane * E;
-  if constexpr (E == 2) {
-    *reinterpret_cast<uint16_t*>(dst) = c[0] | (c[1] << 8);
-  } else {
-#pragma unroll
-    for (int e = 0; e < E; e += 4)
-      *reinterpret_cast<uint32_t*>(dst + e) = c[e] | (c[e + 1] << 8) | (c[e + 2] << 16) | (c[e + 3] << 24);
-  }
-}
 
 __device__ __forceinline__ void write_scale(const PrepArgs& a, int b, int h, int blk, double amax,
                                             bool bad) {
@@ -220,36 +82,134 @@ __device__ __forceinline__ void write_scale(const PrepArgs& a, int b, int h, int
 // the loads and stores): shuffles under a thread-dependent branch compile to
 // WARPSYNC collectives that cost more than the arithmetic.
 
-// 128-row blocks, d <= 128: 16 warps x 8 rows, the transformed block stays in
-// registers between the amax reduction and the encode (one read of the input).
-template <int E>
-__global__ void __launch_bounds__(512) fa3b_fp8_prepare_block128_kernel(const PrepArgs a) {
-  constexpr int RPW = 8;
-  const int blk = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r0 = blk * 128 + warp * RPW;
-  __shared__ double s_amax[16];
-  __shared__ int s_bad[16];
-  double v[RPW][E];
-  double amax = 0.0;
-  bool bad = false;
-  // every row's loads are in flight before any arithmetic; rows past N read as zero
-  RawRow<E> raw[RPW];
+// Quad layout: LPR lanes per row (4 at d <= 128, 8 at d = 256). Lane l owns row
+// l / LPR of its warp's group and the elements [Q (l % LPR), Q (l % LPR) + Q),
+// Q = d / LPR (16 or 32), so log2(Q) butterfly stages run in registers and only
+// log2(LPR) cross lanes (64-bit shuffles within the lane group).
+template <int D>
+struct Quad {
+  static constexpr int LPR = D <= 128 ? 4 : 8;
+  static constexpr int Q = D / LPR;
+  static constexpr int RPW = 32 / LPR;  // rows per warp
+};
+
+template <int D>
+__device__ __forceinline__ void quad_load(const PrepArgs& a, int b, int h, int row, bool valid, int qd,
+                                          double (&v)[Quad<D>::Q]) {
+  constexpr int Q = Quad<D>::Q;
+  const size_t base = b * a.s_sb + static_cast<size_t>(row) * a.s_ss + h * a.s_sh + qd * Q;
+  if (a.src_dtype == FA3B_DTYPE_F32) {
+    uint4 raw[Q / 4];
 #pragma unroll
-  for (int rr = 0; rr < RPW; ++rr) {
-    raw[rr] = RawRow<E>{};
-    if (r0 + rr < a.N) load_raw<E>(a, b, h, r0 + rr, lane, raw[rr]);
+    for (int k = 0; k < Q / 4; ++k)
+      raw[k] = valid ? __ldg(reinterpret_cast<const uint4*>(static_cast<const float*>(a.src) + base) + k)
+                     : make_uint4(0, 0, 0, 0);
+    const uint32_t* u = reinterpret_cast<const uint32_t*>(raw);
+#pragma unroll
+    for (int e = 0; e < Q; ++e) v[e] = __uint_as_float(u[e]);
+  } else {
+    uint4 raw[Q / 8];
+#pragma unroll
+    for (int k = 0; k < Q / 8; ++k)
+      raw[k] = valid ? __ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(a.src) + base) + k)
+                     : make_uint4(0, 0, 0, 0);
+    const uint32_t* u = reinterpret_cast<const uint32_t*>(raw);
+#pragma unroll
+    for (int e = 0; e < Q; ++e) {
+      const uint16_t bits = static_cast<uint16_t>(u[e >> 1] >> (16 * (e & 1)));
+      v[e] = a.src_dtype == FA3B_DTYPE_BF16 ? __uint_as_float(static_cast<uint32_t>(bits) << 16)
+                                            : __half2float(__ushort_as_half(bits));
+    }
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void quad_transform(const PrepArgs& a, int qd, double (&v)[Quad<D>::Q]) {
+  constexpr int Q = Quad<D>::Q, LPR = Quad<D>::LPR;
+  if (!a.hadamard) return;
+  // sign_i = +1 iff bit i of the sign mask is set (elements qd Q .. qd Q + Q - 1)
+  const uint32_t sm = static_cast<uint32_t>(a.signs[(qd * Q) >> 6] >> ((qd * Q) & 63));
+#pragma unroll
+  for (int e = 0; e < Q; ++e)
+    if (!((sm >> e) & 1u)) v[e] = -v[e];
+#pragma unroll
+  for (int len = 1; len < Q; len <<= 1) {
+#pragma unroll
+    for (int e = 0; e < Q; ++e) {
+      if ((e & len) == 0) {
+        const double p = v[e], q = v[e + len];
+        v[e] = p + q;
+        v[e + len] = p - q;
+      }
+    }
   }
 #pragma unroll
-  for (int rr = 0; rr < RPW; ++rr) {
-    unpack_raw<E>(a, raw[rr], v[rr]);
-    transform_row<E>(a, lane, v[rr]);
+  for (int m = 1; m < LPR; m <<= 1) {  // stages len = Q, 2Q, ...: partners within the lane group
+    const double sgn = (qd & m) ? -1.0 : 1.0;
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const double x = fabs(v[rr][e]);
-      bad |= !isfinite(x);
-      amax = fmax(amax, x);
+    for (int e = 0; e < Q; ++e) {
+      const double other = __shfl_xor_sync(0xffffffffu, v[e], m);
+      v[e] = fma(sgn, v[e], other);  // exact product: equals a + b / b - a of the reference
     }
+  }
+  const double norm = 1.0 / sqrt(static_cast<double>(D));
+#pragma unroll
+  for (int e = 0; e < Q; ++e) v[e] *= norm;
+}
+
+template <int D>
+__device__ __forceinline__ void quad_store(const PrepArgs& a, int b, int h, int row, int qd,
+                                           const double (&v)[Quad<D>::Q], double inv) {
+  constexpr int Q = Quad<D>::Q;
+  uint32_t packed[Q / 4];
+  if (a.saturate) {
+#pragma unroll
+    for (int e = 0; e < Q; e += 4) {
+      float f[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {  // FP64 -> FP32 round-to-odd, then hardware RNE to e4m3
+        const double t = v[e + u] * inv;
+        float z = __double2float_rz(t);
+        if (static_cast<double>(z) != t) z = __uint_as_float(__float_as_uint(z) | 1u);
+        f[u] = z;
+      }
+      packed[e >> 2] = ptx::pack_e4m3x4(f[0], f[1], f[2], f[3]);
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < Q; e += 4)
+      packed[e >> 2] = e4m3_code(v[e] * inv, false) | (e4m3_code(v[e + 1] * inv, false) << 8) |
+                       (e4m3_code(v[e + 2] * inv, false) << 16) |
+                       (static_cast<uint32_t>(e4m3_code(v[e + 3] * inv, false)) << 24);
+  }
+  uint4* dst = reinterpret_cast<uint4*>(a.dst + b * a.d_sb + static_cast<size_t>(row) * a.d_ss + h * a.d_sh +
+                                        qd * Q);
+#pragma unroll
+  for (int k = 0; k < Q / 16; ++k)
+    dst[k] = make_uint4(packed[4 * k], packed[4 * k + 1], packed[4 * k + 2], packed[4 * k + 3]);
+}
+
+// 128-row blocks, d = 64 / 128: the 16 warps of quad-layout rows hold the whole
+// transformed block in registers across the amax (one read of the input).
+template <int D>
+__global__ void __launch_bounds__(512) fa3b_fp8_prepare_quad_kernel(const PrepArgs a) {
+  using QD = Quad<D>;
+  const int blk = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, qd = lane % QD::LPR;
+  const int row = blk * 128 + warp * QD::RPW + lane / QD::LPR;
+  const bool valid = row < a.N;
+  __shared__ double s_amax[16];
+  __shared__ int s_bad[16];
+  double v[QD::Q];
+  quad_load<D>(a, b, h, row, valid, qd, v);
+  quad_transform<D>(a, qd, v);
+  double amax = 0.0;
+  bool bad = false;
+#pragma unroll
+  for (int e = 0; e < QD::Q; ++e) {
+    const double x = fabs(v[e]);
+    bad |= !isfinite(x);
+    amax = fmax(amax, x);
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, off));
@@ -268,9 +228,7 @@ __global__ void __launch_bounds__(512) fa3b_fp8_prepare_block128_kernel(const Pr
   }
   if (threadIdx.x == 0) write_scale(a, b, h, blk, amax, bad);
   const double inv = 1.0 / (amax == 0.0 ? 1.0 : amax / 448.0);  // quantize.cpp:25
-#pragma unroll
-  for (int rr = 0; rr < RPW; ++rr)
-    if (r0 + rr < a.N) store_codes<E>(a, b, h, r0 + rr, lane, v[rr], inv);
+  if (valid) quad_store<D>(a, b, h, row, qd, v, inv);
 }
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -293,40 +251,33 @@ __device__ __forceinline__ double ld_cluster_f64(const double* p, uint32_t rank)
 // (the second recomputes the transform; its reads hit L1/L2). A block is split
 // over a cluster of C CTAs whose partial maxima meet through distributed shared
 // memory, so even one scale per (batch, head) keeps C x B x H CTAs busy.
-template <int E, int C>
+template <int D, int C>
 __global__ void __launch_bounds__(256) fa3b_fp8_prepare_kernel(const PrepArgs a) {
-  constexpr int WARPS = 8, RPI = 2;  // rows per warp per iteration
+  using QD = Quad<D>;
+  constexpr int WARPS = 8, ROWS = WARPS * QD::RPW;  // rows per CTA iteration
   const int blk = blockIdx.x / C, part = blockIdx.x % C, h = blockIdx.y, b = blockIdx.z;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, qd = lane % QD::LPR;
   const int rb0 = a.block_rows ? blk * a.block_rows : 0;
   const int rb1 = a.block_rows ? min(a.N, rb0 + a.block_rows) : a.N;
   const int chunk = (rb1 - rb0 + C - 1) / C;
   const int c0 = rb0 + part * chunk, c1 = min(rb1, c0 + chunk);
-  const int iters = c1 > c0 ? (c1 - c0 + WARPS * RPI - 1) / (WARPS * RPI) : 0;
+  const int iters = c1 > c0 ? (c1 - c0 + ROWS - 1) / ROWS : 0;
+  const int rsub = warp * QD::RPW + lane / QD::LPR;
   __shared__ double s_amax[WARPS];
   __shared__ int s_bad[WARPS];
   __shared__ double s_cta[2];  // this CTA's (amax, bad) for the cluster
   double amax = 0.0;
   bool bad = false;
   for (int it = 0; it < iters; ++it) {
-    RawRow<E> raw[RPI];
+    const int row = c0 + it * ROWS + rsub;
+    double v[QD::Q];
+    quad_load<D>(a, b, h, row, row < c1, qd, v);
+    quad_transform<D>(a, qd, v);
 #pragma unroll
-    for (int u = 0; u < RPI; ++u) {
-      const int row = c0 + (it * RPI + u) * WARPS + warp;
-      raw[u] = RawRow<E>{};
-      if (row < c1) load_raw<E>(a, b, h, row, lane, raw[u]);
-    }
-#pragma unroll
-    for (int u = 0; u < RPI; ++u) {
-      double v[E];
-      unpack_raw<E>(a, raw[u], v);
-      transform_row<E>(a, lane, v);
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const double x = fabs(v[e]);
-        bad |= !isfinite(x);
-        amax = fmax(amax, x);
-      }
+    for (int e = 0; e < QD::Q; ++e) {
+      const double x = fabs(v[e]);
+      bad |= !isfinite(x);
+      amax = fmax(amax, x);
     }
   }
 #pragma unroll
@@ -360,27 +311,17 @@ __global__ void __launch_bounds__(256) fa3b_fp8_prepare_kernel(const PrepArgs a)
   if (threadIdx.x == 0 && (C == 1 || cluster_rank() == 0)) write_scale(a, b, h, blk, amax, bad);
   const double inv = 1.0 / (amax == 0.0 ? 1.0 : amax / 448.0);
   for (int it = 0; it < iters; ++it) {
-    RawRow<E> raw[RPI];
-#pragma unroll
-    for (int u = 0; u < RPI; ++u) {
-      const int row = c0 + (it * RPI + u) * WARPS + warp;
-      raw[u] = RawRow<E>{};
-      if (row < c1) load_raw<E>(a, b, h, row, lane, raw[u]);
-    }
-#pragma unroll
-    for (int u = 0; u < RPI; ++u) {
-      const int row = c0 + (it * RPI + u) * WARPS + warp;
-      double v[E];
-      unpack_raw<E>(a, raw[u], v);
-      transform_row<E>(a, lane, v);
-      if (row < c1) store_codes<E>(a, b, h, row, lane, v, inv);
-    }
+    const int row = c0 + it * ROWS + rsub;
+    double v[QD::Q];
+    quad_load<D>(a, b, h, row, row < c1, qd, v);
+    quad_transform<D>(a, qd, v);
+    if (row < c1) quad_store<D>(a, b, h, row, qd, v, inv);
   }
 }
 
-template <int E, int C>
+template <int D, int C>
 cudaError_t launch_two_pass(const PrepArgs& a, dim3 grid, cudaStream_t st) {
-  auto kern = fa3b_fp8_prepare_kernel<E, C>;
+  auto kern = fa3b_fp8_prepare_kernel<D, C>;
   grid.x *= C;
   if constexpr (C == 1) {
     kern<<<grid, 256, 0, st>>>(a);
@@ -401,13 +342,13 @@ cudaError_t launch_two_pass(const PrepArgs& a, dim3 grid, cudaStream_t st) {
   }
 }
 
-template <int E>
+template <int D>
 cudaError_t launch_generic(const PrepArgs& a, dim3 grid, cudaStream_t st) {
   // split each scale block over a cluster when there are too few blocks to fill 148 SMs
   const long long ctas = static_cast<long long>(grid.x) * grid.y * grid.z;
   const int rows = a.block_rows ? a.block_rows : a.N;
-  if (ctas < 296 && rows >= 8 * 256) return launch_two_pass<E, 8>(a, grid, st);
-  return launch_two_pass<E, 1>(a, grid, st);
+  if (ctas < 296 && rows >= 8 * 256) return launch_two_pass<D, 8>(a, grid, st);
+  return launch_two_pass<D, 1>(a, grid, st);
 }
 
 uint64_t mix64(uint64_t z) {  // rng.cpp:15-19
@@ -462,15 +403,15 @@ extern "C" int fa3b_fp8_prepare(const fa3b_fp8_prepare_params* pp) {
   cudaError_t e = cudaSuccess;
   if (p.block_rows == 128 && p.head_dim <= 128) {
     // d = 256 would hold 64 doubles per thread; it takes the two-pass kernel instead
-    switch (p.head_dim) {
-      case 64: fa3b_fp8_prepare_block128_kernel<2><<<grid, 512, 0, st>>>(a); break;
-      default: fa3b_fp8_prepare_block128_kernel<4><<<grid, 512, 0, st>>>(a); break;
-    }
+    if (p.head_dim == 64)
+      fa3b_fp8_prepare_quad_kernel<64><<<grid, 512, 0, st>>>(a);
+    else
+      fa3b_fp8_prepare_quad_kernel<128><<<grid, 512, 0, st>>>(a);
   } else {
     switch (p.head_dim) {
-      case 64: e = launch_generic<2>(a, grid, st); break;
-      case 128: e = launch_generic<4>(a, grid, st); break;
-      default: e = launch_generic<8>(a, grid, st); break;
+      case 64: e = launch_generic<64>(a, grid, st); break;
+      case 128: e = launch_generic<128>(a, grid, st); break;
+      default: e = launch_generic<256>(a, grid, st); break;
     }
     if (e != cudaSuccess) return cuda_fail(e);
   }
