@@ -177,10 +177,12 @@ def test_full_size_against_torch_rows(cuda, D, causal):
 
 
 @pytest.mark.parametrize("B,N,H,Hkv,causal", [(1, 65536, 1, 1, True), (1, 8192, 64, 8, False),
-                                              (64, 256, 8, 8, True)])
+                                              (64, 256, 8, 8, True), (1, 256, 149, 149, True),
+                                              (3, 512, 99, 33, True)])
 def test_extreme_shapes_against_torch_rows(cuda, B, N, H, Hkv, causal):
-    """64k keys (qb grid and LPT order at their largest), C5's 64/8 GQA, and a
-    4096-tile batch x head grid: sampled rows against fp32 torch."""
+    """64k keys, C5's 64/8 GQA, a 4096-item grid, and item counts one past one and
+    two rounds of the 148-CTA persistent grid (causal boustrophedon rounds):
+    sampled rows against fp32 torch."""
     api = _api()
     torch = _torch()
     D = 128
