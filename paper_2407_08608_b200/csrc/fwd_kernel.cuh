@@ -42,9 +42,34 @@
 // s_v is applied in the epilogue. (Folding s_v into P instead costs ~15% RMSE
 // on outlier inputs because small P codes drop into e4m3 subnormals.) Both MMAs run as tcgen05 kind::f8f6f4 with V consumed
 // MN-major straight from the TMA tile (no in-kernel transpose on sm_100a).
+//
+// FP8 with one query tile per CTA (T::P_SMEM; d = 256 and the basic schedule):
+// P goes to a double-buffered 128B-swizzled shared-memory tile and PV is an
+// SS-MMA (at N = 128 exactly the 128 B/clk SS operand rate). S_t is then free as
+// soon as the softmax has it in registers (s_free), so the MMA warp computes
+// S(K_{j+1}) during the softmax of block j — the paper's intra-warpgroup overlap
+// (PAPER.md:307-330), which the TMEM-resident P (aliasing S) rules out. pv_done
+// per P buffer tells the softmax when O may be rescaled and a buffer reused; the
+// MMA warp serves the tiles' s_free / p_full events in arrival order.
 #pragma once
 
 #include "sm100_ptx.cuh"
+
+// Register rebalancing: with FA3B_FWD_REGS = R > 0 the producer / MMA warps get
+// two idle companions (one full warpgroup) that drop to 56 registers with
+// setmaxnreg so the softmax warpgroups can rise from the launch cap (96) to R.
+#ifndef FA3B_FWD_REGS
+#define FA3B_FWD_REGS 0
+#endif
+#ifndef FA3B_PSMEM_NT
+#define FA3B_PSMEM_NT 1
+#endif
+#ifndef FA3B_MMA_POLL_NS
+#define FA3B_MMA_POLL_NS 64
+#endif
+#ifndef FA3B_FWD_OREGS
+#define FA3B_FWD_OREGS 56
+#endif
 
 namespace fa3b {
 
@@ -100,7 +125,10 @@ struct FwdArgs {
   const float* v_scale;
   int q_blocked, kv_blocked;
   float fp8_thr;         // lazy-rescale threshold (log2) for the e4m3 P
+  float fp8_pmul, fp8_inv_pmul, fp8_lpm;  // 448 / 2^thr, its inverse and log2 (host-computed)
 };
+__device__ __forceinline__ int fwd_seqlen(const FwdArgs& a) { return a.N; }
+
 
 // CPS_ = CTAs per SM. CPS = 2 (one query tile per CTA, d <= 128) gives the
 // tensor core two independent tiles per SM from two CTAs instead of one CTA's
@@ -117,18 +145,28 @@ struct FwdTraits {
   static constexpr int CHUNK_ELEMS = 128 / EB;
   static constexpr int CHUNKS = D / CHUNK_ELEMS;
   static constexpr int TILE_BYTES = CHUNKS * CHUNK_BYTES;
+  // FP8 (one CTA per SM): P goes to shared memory (double-buffered per tile) and PV
+  // is an SS-MMA, so S(K_{j+1}) can overwrite S_t as soon as S_j is in registers
+  // (one query tile per CTA: with the NT = 2 ping-pong the early S only makes the two
+  // tiles' softmax phases collide, measured slower at d = 128)
+  static constexpr bool P_SMEM = EB == 1 && CPS == 1 && NT == FA3B_PSMEM_NT;
+  static constexpr int P_BYTES = 128 * 128;  // one e4m3 P tile, 128 rows x 128 B
   static constexpr int STAGES = CPS == 2 ? (TILE_BYTES <= 16384 ? 4 : 2)
+                                : P_SMEM ? (TILE_BYTES <= 16384 ? 6 : 4)
                                          : (TILE_BYTES <= 16384 ? 8 : (TILE_BYTES <= 32768 ? 4 : 2));
   // two softmax warpgroups per query tile, each owning 64 of the 128 columns
-  static constexpr int NUM_THREADS = NT * 256 + 64;
+  static constexpr int SOFT_REGS = (CPS == 1 && NT == 2) ? FA3B_FWD_REGS : 0;
+  static constexpr int NUM_THREADS = NT * 256 + (SOFT_REGS > 0 ? 128 : 64);
   static constexpr int LOAD_WARP = NT * 8;
   static constexpr int MMA_WARP = NT * 8 + 1;
   static constexpr uint32_t TMEM_COLS = CPS == 2 ? 256 : 512;
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_KV = NT * TILE_BYTES;
-  static constexpr int OFF_BAR = OFF_KV + STAGES * TILE_BYTES;
-  // q_full, kv_full[S], kv_empty[S], s_full[NT], p_full[NT], o_full[NT], q_empty
-  static constexpr int NUM_BARS = 2 + 2 * STAGES + 3 * NT;
+  static constexpr int OFF_P = OFF_KV + STAGES * TILE_BYTES;  // [NT][2 buf] P tiles (P_SMEM)
+  static constexpr int OFF_BAR = OFF_P + (P_SMEM ? NT * 2 * P_BYTES : 0);
+  // q_full, kv_full[S], kv_empty[S], s_full[NT], p_full[NT], o_full[NT], q_empty,
+  // s_free[NT], pv_done[NT][2 P buffers]
+  static constexpr int NUM_BARS = 2 + 2 * STAGES + 6 * NT;
   // row-max / row-sum exchange between the two column halves: [NT][2 buf][2 half][128]
   static constexpr int OFF_XCH = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr int SMEM_BYTES = OFF_XCH + NT * 2 * 2 * 128 * 4 + 1024;
@@ -164,6 +202,8 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
   uint64_t* p_full = s_full + NT;
   uint64_t* o_full = p_full + NT;
   uint64_t* q_empty = o_full + NT;  // the Q tiles of a work item are consumed
+  uint64_t* s_free = q_empty + 1;   // P_SMEM: S_t is in registers (8 softmax warps)
+  uint64_t* pv_done = s_free + NT;  // P_SMEM: [t][buf] PV of tile t from P buffer buf complete
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + T::NUM_BARS);
 
   const int warp = static_cast<int>(ptx::warp_id());
@@ -177,11 +217,14 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
   // Non-causal: query blocks of one head adjacent (K/V reuse in L2). Causal:
   // longest first across all heads (query blocks from the bottom of the mask up,
   // every head at each step), so the static round-robin stays balanced.
-  const int N = args.N;
-  const int nqb = (N + NT * 128 - 1) / (NT * 128);
-  const int HB = args.H * args.B;
-  const int num_items = nqb * HB;
-  const int nkv = (N + 127) / 128;
+  // (kept as expressions of the kernel arguments, not values computed before the
+  // role split: each role re-derives them from the constant bank instead of
+  // carrying them in registers, which the 96-register softmax cannot afford)
+#define N (fwd_seqlen(args))
+#define nqb ((fwd_seqlen(args) + NT * 128 - 1) / (NT * 128))
+#define HB (args.H * args.B)
+#define num_items (nqb * HB)
+#define nkv ((fwd_seqlen(args) + 127) / 128)
   struct Item {
     int qb, h, b, hkv, q_base, n_max;
     int n_t[NT];
@@ -221,6 +264,9 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
         ptx::mbar_init(&s_full[t], 1);
         ptx::mbar_init(&p_full[t], 8);  // one arrival per softmax warp
         ptx::mbar_init(&o_full[t], 1);
+        ptx::mbar_init(&s_free[t], 8);
+        ptx::mbar_init(&pv_done[2 * t], 1);
+        ptx::mbar_init(&pv_done[2 * t + 1], 1);
       }
       ptx::mbar_init(q_empty, 1);
       ptx::fence_mbar_init();
@@ -236,8 +282,15 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  // TMEM base: re-read from shared memory inside each role (a value carried across
+  // the role split is one more register the softmax would spill)
+#define FA3B_TMEM_BASE (*reinterpret_cast<volatile uint32_t*>(tmem_slot))
 
+  if constexpr (T::SOFT_REGS > 0) {
+    static_assert(NT * 8 * T::SOFT_REGS + 4 * FA3B_FWD_OREGS <= (T::NUM_THREADS / 32) * 96, "register pool");
+    if (warp >= NT * 8)
+      ptx::setmaxnreg_dec<FA3B_FWD_OREGS>();
+  }
   if (warp == T::LOAD_WARP) {
     // ------------------------------------------------------------ producer
     if (ptx::elect_one()) {
@@ -284,6 +337,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
   } else if (warp == T::MMA_WARP) {
     // ------------------------------------------------------------ MMA issuer
     if (ptx::elect_one()) {
+      const uint32_t tmem = FA3B_TMEM_BASE;
       const uint32_t q_addr = ptx::smem_u32(smem + T::OFF_Q);
       const uint32_t kv_addr = ptx::smem_u32(smem + T::OFF_KV);
       // one MMA consumes 32 bytes of K: 16 f16/bf16 or 32 e4m3 elements
@@ -318,8 +372,106 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       int kvi = 0;  // ring position of this item's K_0
       int itl = 0;
       int pc[NT];   // p_full phases consumed per tile
+      int fc[NT];   // s_free phases consumed per tile (P_SMEM)
 #pragma unroll
-      for (int t = 0; t < NT; ++t) pc[t] = 0;
+      for (int t = 0; t < NT; ++t) pc[t] = fc[t] = 0;
+      if constexpr (T::P_SMEM) {
+        // P_t in shared memory, buffer = PV count & 1 (K-major, 128B swizzle)
+        const uint32_t p_addr = ptx::smem_u32(smem + T::OFF_P);
+        auto issue_pv_ss = [&](int t, int slot, bool acc, int buf) {
+#pragma unroll
+          for (int k = 0; k < 128 / KSTEP; ++k) {
+            const uint64_t bd = ptx::sw128_desc(kv_addr + slot * T::TILE_BYTES + k * KSTEP * 128,
+                                                T::CHUNK_BYTES, 1024);
+            const uint64_t ad = ptx::sw128_desc(p_addr + (2 * t + buf) * T::P_BYTES + k * 32, 16, 1024);
+            ptx::mma_f8_ss(tmem + T::o_col(t), ad, bd, idesc_pv, (acc || k > 0) ? 1u : 0u);
+          }
+        };
+        // Per item: S(K_0) ; { S(K_{j+1}) once S_j is in registers ; PV(V_j) once P_j is
+        // in shared memory }_j. pv_done tells the softmax when O may be rescaled and
+        // which P buffer is free again.
+        for (int lin = item_of(0); lin < num_items; lin = item_of(++itl)) {
+          const Item w = decode(lin);
+          ptx::mbar_wait(q_full, itl & 1);
+          {
+            const int slot0 = kvi % T::STAGES;
+            ptx::mbar_wait(&kv_full[slot0], (kvi / T::STAGES) & 1);
+            ptx::tc_fence_after();
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+              if (w.n_t[t] == 0) continue;
+              issue_qk(t, slot0);
+              ptx::mma_commit(&s_full[t]);
+            }
+            ptx::mma_commit(&kv_empty[slot0]);
+          }
+          // Event loop over the tiles: each tile alternates s_free(j) -> S(K_{j+1}) and
+          // p_full(j) -> PV(V_j); whichever tile is ready is served first, so one tile's
+          // softmax never waits behind the other's. A ring slot is released by the last
+          // tile that reads it.
+          int jn[NT];    // next PV block per tile
+          bool sd[NT];   // S(K_{jn+1}) issued (or not needed)
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            jn[t] = 0;
+            sd[t] = w.n_t[t] <= 1;
+          }
+          auto k_done = [&](int u, int i) {  // tile u no longer needs K_i
+            return w.n_t[u] <= i || jn[u] >= i || (jn[u] == i - 1 && sd[u]);
+          };
+          auto v_done = [&](int u, int i) { return w.n_t[u] <= i || jn[u] > i; };
+          for (;;) {
+            bool left = false, moved = false;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+              const int j = jn[t];
+              if (j >= w.n_t[t]) continue;
+              left = true;
+              if (!sd[t]) {
+                const int item_k = kvi + 2 * j + 2, slot_k = item_k % T::STAGES;
+                if (ptx::mbar_test(&s_free[t], fc[t] & 1) &&
+                    ptx::mbar_test(&kv_full[slot_k], (item_k / T::STAGES) & 1)) {
+                  ++fc[t];
+                  ptx::tc_fence_after();
+                  issue_qk(t, slot_k);
+                  ptx::mma_commit(&s_full[t]);
+                  sd[t] = true;
+                  moved = true;
+                  bool last = true;
+#pragma unroll
+                  for (int u = 0; u < NT; ++u) last = last && (u == t || k_done(u, j + 1));
+                  if (last) ptx::mma_commit(&kv_empty[slot_k]);
+                }
+              }
+              if (sd[t]) {
+                const int item_v = kvi + 2 * j + 1, slot_v = item_v % T::STAGES;
+                if (ptx::mbar_test(&p_full[t], pc[t] & 1) &&
+                    ptx::mbar_test(&kv_full[slot_v], (item_v / T::STAGES) & 1)) {
+                  if (itl == 0) FA3B_TP(t, j, 6);
+                  const int buf = pc[t]++ & 1;
+                  ptx::tc_fence_after();
+                  issue_pv_ss(t, slot_v, j > 0, buf);
+                  ptx::mma_commit(&pv_done[2 * t + buf]);
+                  if (j + 1 == w.n_t[t]) ptx::mma_commit(&o_full[t]);
+                  jn[t] = j + 1;
+                  sd[t] = j + 2 >= w.n_t[t];
+                  moved = true;
+                  bool last = true;
+#pragma unroll
+                  for (int u = 0; u < NT; ++u) last = last && (u == t || v_done(u, j));
+                  if (last) ptx::mma_commit(&kv_empty[slot_v]);
+                }
+              }
+            }
+            if (!left) break;
+            // back off between empty polls: the spinning thread shares its SM
+            // sub-partition's issue slots with two softmax warps
+            if (!moved) __nanosleep(FA3B_MMA_POLL_NS);
+          }
+          ptx::mma_commit(q_empty);
+          kvi += 2 * w.n_max;
+        }
+      } else
       for (int lin = item_of(0); lin < num_items; lin = item_of(++itl)) {
         const Item w = decode(lin);
         ptx::mbar_wait(q_full, itl & 1);
@@ -366,8 +518,10 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
         kvi += 2 * w.n_max;
       }
     }
-  } else {
+  } else if (warp < NT * 8) {
     // ------------------------------------------------------------ softmax
+    if constexpr (T::SOFT_REGS > 0) ptx::setmaxnreg_inc<T::SOFT_REGS>();
+    const uint32_t tmem = FA3B_TMEM_BASE;
     const int t = warp >> 3;             // query tile
     const int hh = (warp >> 2) & 1;      // column half of S / O
     const int r = ((warp & 3) << 5) | static_cast<int>(ptx::lane_id());  // row == TMEM lane
@@ -377,6 +531,9 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
     float* xch = reinterpret_cast<float*>(smem + T::OFF_XCH) + t * 512;  // [2 buf][2 half][128]
     const uint32_t bar_id = 1 + t;
     int sc = 0, xc = 0, oc = 0;  // s_full / exchange-buffer / o_full uses so far
+    // P_SMEM: P tile #g of this tile goes to buffer g & 1; g = sc - 1 inside an iteration
+    // P_SMEM: this thread's 64 bytes of row r (16B chunks 4 hh .. 4 hh + 3, swizzled)
+    uint8_t* p_row = smem + T::OFF_P + 2 * t * T::P_BYTES + r * 128;
     int itl = 0;
     for (int lin = item_of(0); lin < num_items; lin = item_of(++itl)) {
     const Item w = decode(lin);
@@ -386,35 +543,31 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
     constexpr int HC = 64;               // columns per half
     constexpr int DH = D / 2;            // O columns per half
     float sl2 = args.scale_log2;
-    float thr = 8.f;
+    const float thr = FP8 ? args.fp8_thr : 8.f;
     float out_scale = 1.f;
-    const float* kscale = nullptr;
-    const float* vscale = nullptr;
+    int ks_base = 0;  // FP8: index of this (batch, kv head)'s first K / V block scale
     if constexpr (FP8) {
       const size_t hq = static_cast<size_t>(b) * args.H + h;
       const size_t hk = static_cast<size_t>(b) * args.Hkv + hkv;
       const int nqb_all = (N + 127) / 128;
       sl2 *= args.q_blocked ? args.q_scale[hq * nqb_all + q_base / 128 + t] : args.q_scale[hq];
-      kscale = args.kv_blocked ? args.k_scale + hk * nkv : args.k_scale + hk;
-      vscale = args.kv_blocked ? args.v_scale + hk * nkv : args.v_scale + hk;
-      thr = args.fp8_thr;
+      ks_base = static_cast<int>(args.kv_blocked ? hk * nkv : hk);
     }
     float v_cur = 0.f;  // V scale the O accumulator is expressed in (FP8)
     float m_use = -INFINITY;  // running max in use, scaled log2 units (same in both halves)
     float l = 0.f;            // this half's share of the row sum
     // FP8: e4m3 codes of P are P * 448 / 2^thr; exp2(x + log2 pmul) produces them directly
-    const float pmul = FP8 ? 448.f * ptx::ex2(-thr) : 1.f;
-    const float inv_pmul = FP8 ? 1.f / pmul : 1.f;
-    const float lpm = FP8 ? __log2f(pmul) : 0.f;
+    const float inv_pmul = FP8 ? args.fp8_inv_pmul : 1.f;
+    const float lpm = FP8 ? args.fp8_lpm : 0.f;
 #ifndef FA3B_FP8_PREFETCH
-#define FA3B_FP8_PREFETCH 0
+#define FA3B_FP8_PREFETCH 1
 #endif
     // per-block K / V scales of the next block are fetched one iteration ahead
     float ks_next = 1.f, vs_next = 1.f;
     if constexpr (FP8) {
       if (nt > 0) {
-        ks_next = kscale[0];
-        vs_next = vscale[0];
+        ks_next = args.k_scale[ks_base];
+        vs_next = args.v_scale[ks_base];
       }
     }
     for (int j = 0; j < nt; ++j) {
@@ -425,12 +578,12 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
         slj = sl2 * ks_next;
         const float vs = vs_next;
         if (args.kv_blocked && j + 1 < nt) {
-          ks_next = kscale[j + 1];
-          vs_next = vscale[j + 1];
+          ks_next = args.k_scale[ks_base + j + 1];
+          vs_next = args.v_scale[ks_base + j + 1];
         }
 #else
-        slj = sl2 * kscale[args.kv_blocked ? j : 0];
-        const float vs = vscale[args.kv_blocked ? j : 0];
+        slj = sl2 * args.k_scale[ks_base + (args.kv_blocked ? j : 0)];
+        const float vs = args.v_scale[ks_base + (args.kv_blocked ? j : 0)];
 #endif
         if (vs != v_cur) {
           vfac = v_cur / vs;  // 0 on the first block: O is empty
@@ -463,6 +616,13 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
         }
       };
       load_s();
+      if constexpr (T::P_SMEM) {
+        if (j + 1 < nt) {  // S_t may be overwritten by S(K_{j+1})
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (ptx::lane_id() == 0) ptx::mbar_arrive(&s_free[t]);
+        }
+      }
       if (tr) FA3B_TP(t, j, 2);
       // half-row max: FMNMX3 over 4 independent chains, then swap with the other half
       float a0 = s[0], a1 = s[1], a2 = s[2], a3 = s[3];
@@ -484,6 +644,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       constexpr int NPK = FP8 ? 16 : 32;
       uint32_t pk[NPK];
       float psum = 0.f;
+      uint8_t* p_dst = p_row + ((sc - 1) & 1) * T::P_BYTES;  // P_SMEM
       auto exp_half = [&](float msub) {
         const float2 sc2 = make_float2(slj, slj), nm2 = make_float2(lpm - msub, lpm - msub);
         float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
@@ -505,6 +666,13 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
               pk[i >> 1] = ptx::pack_e4m3x4(prev.x, prev.y, pp.x, pp.y);
             else
               prev = pp;
+            if constexpr (T::P_SMEM) {
+              if ((i & 7) == 7) {  // 16 codes = one 16-byte chunk of the swizzled row
+                const int c = i >> 3;
+                *reinterpret_cast<uint4*>(p_dst + (((4 * hh + c) ^ (r & 7)) << 4)) =
+                    make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+              }
+            }
           } else {
             pk[i] = BF16 ? ptx::pack_bf16(pp.x, pp.y) : ptx::pack_f16(pp.x, pp.y);
           }
@@ -519,8 +687,17 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       const bool resc = m_new > m_use + thr;
       const float m_cur = resc ? m_new : m_use;
       const float factor = resc ? ptx::ex2(m_use - m_new) : 1.f;
+      if constexpr (T::P_SMEM) {
+        // P buffer g & 1 (g = sc - 1) is free once PV #(g - 2) (same buffer) has completed
+        if (sc >= 3) ptx::mbar_wait(&pv_done[2 * t + ((sc - 1) & 1)], ((sc - 3) >> 1) & 1);
+      }
       exp_half((m_cur == -INFINITY) ? 0.f : m_cur);
-      if constexpr (FP8)
+      if constexpr (T::P_SMEM) {
+        ptx::fence_proxy_async_smem();
+        // O_t may be rescaled once PV #(pg - 1) has completed (the previous item's
+        // last PV was covered by the o_full wait of its epilogue)
+        if (j > 0) ptx::mbar_wait(&pv_done[2 * t + (sc & 1)], ((sc - 2) >> 1) & 1);
+      } else if constexpr (FP8)
         ptx::tmem_st16(tS + 16 * hh, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
       else
         ptx::tmem_st32(tS + 32 * hh, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
@@ -611,8 +788,15 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
 #endif
   if (warp == T::MMA_WARP) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<T::TMEM_COLS>(tmem);
+    ptx::tmem_dealloc<T::TMEM_COLS>(FA3B_TMEM_BASE);
   }
 }
+
+#undef FA3B_TMEM_BASE
+#undef N
+#undef nqb
+#undef HB
+#undef num_items
+#undef nkv
 
 }  // namespace fa3b
