@@ -29,12 +29,16 @@ float fp8_threshold(bool kv_blocked) {
   return kv_blocked ? 0.f : 4.f;
 }
 
+#ifndef FA3B_FWD_EMU_S2
+#define FA3B_FWD_EMU_S2 3
+#endif
+
 template <int D, int NT, bool CAUSAL, int CPS = 1>
 int launch(const fa3b_fwd_params& p, cudaStream_t stream) {
   using T = FwdTraits<D, NT, 1, CPS>;
-  // one query tile per CTA (P in shared memory, S fetched early): the softmax has the
-  // SM to itself, so a third of the exp2 pairs go to the FMA pipe instead of a quarter
-  constexpr int EMU = T::P_SMEM ? 3 : FA3B_FWD_EMU;
+  // one query tile per CTA with S fetched early (S2): the softmax has the SM to
+  // itself, so a third of the exp2 pairs go to the FMA pipe instead of a quarter
+  constexpr int EMU = T::S2 ? FA3B_FWD_EMU_S2 : FA3B_FWD_EMU;
   auto kern = fa3b_fwd_kernel<D, NT, CAUSAL, KIND_E4M3, CPS, EMU>;
   int rc = ensure_smem_attr(reinterpret_cast<const void*>(kern), T::SMEM_BYTES);
   if (rc != FA3B_OK) return rc;

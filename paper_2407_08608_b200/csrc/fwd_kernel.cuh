@@ -43,14 +43,13 @@
 // on outlier inputs because small P codes drop into e4m3 subnormals.) Both MMAs run as tcgen05 kind::f8f6f4 with V consumed
 // MN-major straight from the TMA tile (no in-kernel transpose on sm_100a).
 //
-// FP8 with one query tile per CTA (T::P_SMEM; d = 256 and the basic schedule):
-// P goes to a double-buffered 128B-swizzled shared-memory tile and PV is an
-// SS-MMA (at N = 128 exactly the 128 B/clk SS operand rate). S_t is then free as
-// soon as the softmax has it in registers (s_free), so the MMA warp computes
-// S(K_{j+1}) during the softmax of block j — the paper's intra-warpgroup overlap
-// (PAPER.md:307-330), which the TMEM-resident P (aliasing S) rules out. pv_done
-// per P buffer tells the softmax when O may be rescaled and a buffer reused; the
-// MMA warp serves the tiles' s_free / p_full events in arrival order.
+// One query tile per CTA (d = 256 and the basic schedule; T::S2): TMEM has
+// room for a second S buffer after O, so the MMA warp computes S(K_{j+1}) while
+// the softmax still works on S_j / P_j — the paper's intra-warpgroup overlap
+// (PAPER.md:307-330). Order S_0 ; S_1 ; { PV_j ; S_{j+2} }_j, S_{j+2} reusing
+// S_j's columns after PV_j has read P_j; pv_done tells the softmax when O may be
+// rescaled. Enabled for e4m3 only: at bf16 d = 256 the two-stage K/V ring
+// (64 KB tiles) cannot feed the earlier K loads (measured slower).
 #pragma once
 
 #include "sm100_ptx.cuh"
@@ -61,11 +60,8 @@
 #ifndef FA3B_FWD_REGS
 #define FA3B_FWD_REGS 0
 #endif
-#ifndef FA3B_PSMEM_NT
-#define FA3B_PSMEM_NT 1
-#endif
-#ifndef FA3B_MMA_POLL_NS
-#define FA3B_MMA_POLL_NS 64
+#ifndef FA3B_FWD_S2
+#define FA3B_FWD_S2 1
 #endif
 #ifndef FA3B_FWD_OREGS
 #define FA3B_FWD_OREGS 56
@@ -145,14 +141,7 @@ struct FwdTraits {
   static constexpr int CHUNK_ELEMS = 128 / EB;
   static constexpr int CHUNKS = D / CHUNK_ELEMS;
   static constexpr int TILE_BYTES = CHUNKS * CHUNK_BYTES;
-  // FP8 (one CTA per SM): P goes to shared memory (double-buffered per tile) and PV
-  // is an SS-MMA, so S(K_{j+1}) can overwrite S_t as soon as S_j is in registers
-  // (one query tile per CTA: with the NT = 2 ping-pong the early S only makes the two
-  // tiles' softmax phases collide, measured slower at d = 128)
-  static constexpr bool P_SMEM = EB == 1 && CPS == 1 && NT == FA3B_PSMEM_NT;
-  static constexpr int P_BYTES = 128 * 128;  // one e4m3 P tile, 128 rows x 128 B
   static constexpr int STAGES = CPS == 2 ? (TILE_BYTES <= 16384 ? 4 : 2)
-                                : P_SMEM ? (TILE_BYTES <= 16384 ? 6 : 4)
                                          : (TILE_BYTES <= 16384 ? 8 : (TILE_BYTES <= 32768 ? 4 : 2));
   // two softmax warpgroups per query tile, each owning 64 of the 128 columns
   static constexpr int SOFT_REGS = (CPS == 1 && NT == 2) ? FA3B_FWD_REGS : 0;
@@ -160,13 +149,14 @@ struct FwdTraits {
   static constexpr int LOAD_WARP = NT * 8;
   static constexpr int MMA_WARP = NT * 8 + 1;
   static constexpr uint32_t TMEM_COLS = CPS == 2 ? 256 : 512;
+  // one query tile per CTA, e4m3: a second S buffer after O (see the header)
+  static constexpr bool S2 = NT == 1 && CPS == 1 && EB == 1 && FA3B_FWD_S2;
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_KV = NT * TILE_BYTES;
-  static constexpr int OFF_P = OFF_KV + STAGES * TILE_BYTES;  // [NT][2 buf] P tiles (P_SMEM)
-  static constexpr int OFF_BAR = OFF_P + (P_SMEM ? NT * 2 * P_BYTES : 0);
-  // q_full, kv_full[S], kv_empty[S], s_full[NT], p_full[NT], o_full[NT], q_empty,
-  // s_free[NT], pv_done[NT][2 P buffers]
-  static constexpr int NUM_BARS = 2 + 2 * STAGES + 6 * NT;
+  static constexpr int OFF_BAR = OFF_KV + STAGES * TILE_BYTES;
+  // q_full, kv_full[S], kv_empty[S], s_full[NT + 1], p_full[NT], o_full[NT], q_empty,
+  // pv_done (s_full[NT] and pv_done serve S2)
+  static constexpr int NUM_BARS = 4 + 2 * STAGES + 3 * NT;
   // row-max / row-sum exchange between the two column halves: [NT][2 buf][2 half][128]
   static constexpr int OFF_XCH = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr int SMEM_BYTES = OFF_XCH + NT * 2 * 2 * 128 * 4 + 1024;
@@ -174,6 +164,7 @@ struct FwdTraits {
   static_assert(CPS == 1 || (NT == 1 && SMEM_BYTES * 2 <= 233472), "two CTAs per SM");
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
   __host__ __device__ static constexpr int s_col(int t) { return t * 128; }
+  __host__ __device__ static constexpr int s2_col(int buf) { return buf ? 128 + D : 0; }
   __host__ __device__ static constexpr int o_col(int t) { return NT * 128 + t * D; }
 };
 
@@ -199,11 +190,10 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
   uint64_t* kv_full = bars + 1;
   uint64_t* kv_empty = kv_full + T::STAGES;
   uint64_t* s_full = kv_empty + T::STAGES;
-  uint64_t* p_full = s_full + NT;
+  uint64_t* p_full = s_full + NT + 1;  // (s_full[NT] is the S2 second buffer's)
   uint64_t* o_full = p_full + NT;
   uint64_t* q_empty = o_full + NT;  // the Q tiles of a work item are consumed
-  uint64_t* s_free = q_empty + 1;   // P_SMEM: S_t is in registers (8 softmax warps)
-  uint64_t* pv_done = s_free + NT;  // P_SMEM: [t][buf] PV of tile t from P buffer buf complete
+  uint64_t* pv_done = q_empty + 1;  // S2: PV complete
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + T::NUM_BARS);
 
   const int warp = static_cast<int>(ptx::warp_id());
@@ -262,13 +252,12 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       }
       for (int t = 0; t < NT; ++t) {
         ptx::mbar_init(&s_full[t], 1);
+        if (t == 0) ptx::mbar_init(&s_full[NT], 1);
         ptx::mbar_init(&p_full[t], 8);  // one arrival per softmax warp
         ptx::mbar_init(&o_full[t], 1);
-        ptx::mbar_init(&s_free[t], 8);
-        ptx::mbar_init(&pv_done[2 * t], 1);
-        ptx::mbar_init(&pv_done[2 * t + 1], 1);
       }
       ptx::mbar_init(q_empty, 1);
+      ptx::mbar_init(pv_done, 1);
       ptx::fence_mbar_init();
     }
     __syncwarp();
@@ -342,19 +331,19 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       const uint32_t kv_addr = ptx::smem_u32(smem + T::OFF_KV);
       // one MMA consumes 32 bytes of K: 16 f16/bf16 or 32 e4m3 elements
       constexpr int KSTEP = 32 / T::EB;
-      auto issue_qk = [&](int t, int slot) {
+      auto issue_qk = [&](int t, int slot, int scol) {
 #pragma unroll
         for (int k = 0; k < D / KSTEP; ++k) {
           const uint32_t off = (k >> 2) * T::CHUNK_BYTES + (k & 3) * 32;
           const uint64_t a = ptx::sw128_desc(q_addr + t * T::TILE_BYTES + off, 16, 1024);
           const uint64_t bd = ptx::sw128_desc(kv_addr + slot * T::TILE_BYTES + off, 16, 1024);
           if constexpr (FP8)
-            ptx::mma_f8_ss(tmem + T::s_col(t), a, bd, idesc_qk, k > 0 ? 1u : 0u);
+            ptx::mma_f8_ss(tmem + scol, a, bd, idesc_qk, k > 0 ? 1u : 0u);
           else
-            ptx::mma_f16_ss(tmem + T::s_col(t), a, bd, idesc_qk, k > 0 ? 1u : 0u);
+            ptx::mma_f16_ss(tmem + scol, a, bd, idesc_qk, k > 0 ? 1u : 0u);
         }
       };
-      auto issue_pv = [&](int t, int slot, bool acc) {
+      auto issue_pv = [&](int t, int slot, bool acc, int scol) {
 #pragma unroll
         for (int k = 0; k < 128 / KSTEP; ++k) {
           // B = V, MN-major: KSTEP kv rows of 128 bytes per step
@@ -362,114 +351,59 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
                                               T::CHUNK_BYTES, 1024);
           // A = P in TMEM: KSTEP elements = 8 columns of 32 bits
           if constexpr (FP8)
-            ptx::mma_f8_ts(tmem + T::o_col(t), tmem + T::s_col(t) + k * 8, bd, idesc_pv,
+            ptx::mma_f8_ts(tmem + T::o_col(t), tmem + scol + k * 8, bd, idesc_pv,
                            (acc || k > 0) ? 1u : 0u);
           else
-            ptx::mma_f16_ts(tmem + T::o_col(t), tmem + T::s_col(t) + k * 8, bd, idesc_pv,
+            ptx::mma_f16_ts(tmem + T::o_col(t), tmem + scol + k * 8, bd, idesc_pv,
                             (acc || k > 0) ? 1u : 0u);
         }
       };
       int kvi = 0;  // ring position of this item's K_0
       int itl = 0;
       int pc[NT];   // p_full phases consumed per tile
-      int fc[NT];   // s_free phases consumed per tile (P_SMEM)
 #pragma unroll
-      for (int t = 0; t < NT; ++t) pc[t] = fc[t] = 0;
-      if constexpr (T::P_SMEM) {
-        // P_t in shared memory, buffer = PV count & 1 (K-major, 128B swizzle)
-        const uint32_t p_addr = ptx::smem_u32(smem + T::OFF_P);
-        auto issue_pv_ss = [&](int t, int slot, bool acc, int buf) {
-#pragma unroll
-          for (int k = 0; k < 128 / KSTEP; ++k) {
-            const uint64_t bd = ptx::sw128_desc(kv_addr + slot * T::TILE_BYTES + k * KSTEP * 128,
-                                                T::CHUNK_BYTES, 1024);
-            const uint64_t ad = ptx::sw128_desc(p_addr + (2 * t + buf) * T::P_BYTES + k * 32, 16, 1024);
-            ptx::mma_f8_ss(tmem + T::o_col(t), ad, bd, idesc_pv, (acc || k > 0) ? 1u : 0u);
-          }
+      for (int t = 0; t < NT; ++t) pc[t] = 0;
+      if constexpr (T::S2) {
+        // One tile, two S buffers (global S index g -> buffer g & 1):
+        //   S_0 ; S_1 ; { PV_j ; S_{j+2} }_j
+        // S_{j+2} reuses S_j's columns (P_j), issued after PV_j which reads them.
+        int gs = 0;  // S GEMMs issued so far
+        auto s_issue = [&](int slot) {
+          issue_qk(0, slot, T::s2_col(gs & 1));
+          ptx::mma_commit(&s_full[(gs & 1) ? NT : 0]);
+          ++gs;
         };
-        // Per item: S(K_0) ; { S(K_{j+1}) once S_j is in registers ; PV(V_j) once P_j is
-        // in shared memory }_j. pv_done tells the softmax when O may be rescaled and
-        // which P buffer is free again.
         for (int lin = item_of(0); lin < num_items; lin = item_of(++itl)) {
           const Item w = decode(lin);
+          const int n = w.n_t[0];
           ptx::mbar_wait(q_full, itl & 1);
-          {
-            const int slot0 = kvi % T::STAGES;
-            ptx::mbar_wait(&kv_full[slot0], (kvi / T::STAGES) & 1);
+          const int g0 = gs;  // global index of this item's S_0
+          for (int j = 0; j < 2 && j < n; ++j) {
+            const int item_k = kvi + 2 * j;
+            ptx::mbar_wait(&kv_full[item_k % T::STAGES], (item_k / T::STAGES) & 1);
             ptx::tc_fence_after();
-#pragma unroll
-            for (int t = 0; t < NT; ++t) {
-              if (w.n_t[t] == 0) continue;
-              issue_qk(t, slot0);
-              ptx::mma_commit(&s_full[t]);
-            }
-            ptx::mma_commit(&kv_empty[slot0]);
+            s_issue(item_k % T::STAGES);
+            ptx::mma_commit(&kv_empty[item_k % T::STAGES]);
           }
-          // Event loop over the tiles: each tile alternates s_free(j) -> S(K_{j+1}) and
-          // p_full(j) -> PV(V_j); whichever tile is ready is served first, so one tile's
-          // softmax never waits behind the other's. A ring slot is released by the last
-          // tile that reads it.
-          int jn[NT];    // next PV block per tile
-          bool sd[NT];   // S(K_{jn+1}) issued (or not needed)
-#pragma unroll
-          for (int t = 0; t < NT; ++t) {
-            jn[t] = 0;
-            sd[t] = w.n_t[t] <= 1;
-          }
-          auto k_done = [&](int u, int i) {  // tile u no longer needs K_i
-            return w.n_t[u] <= i || jn[u] >= i || (jn[u] == i - 1 && sd[u]);
-          };
-          auto v_done = [&](int u, int i) { return w.n_t[u] <= i || jn[u] > i; };
-          for (;;) {
-            bool left = false, moved = false;
-#pragma unroll
-            for (int t = 0; t < NT; ++t) {
-              const int j = jn[t];
-              if (j >= w.n_t[t]) continue;
-              left = true;
-              if (!sd[t]) {
-                const int item_k = kvi + 2 * j + 2, slot_k = item_k % T::STAGES;
-                if (ptx::mbar_test(&s_free[t], fc[t] & 1) &&
-                    ptx::mbar_test(&kv_full[slot_k], (item_k / T::STAGES) & 1)) {
-                  ++fc[t];
-                  ptx::tc_fence_after();
-                  issue_qk(t, slot_k);
-                  ptx::mma_commit(&s_full[t]);
-                  sd[t] = true;
-                  moved = true;
-                  bool last = true;
-#pragma unroll
-                  for (int u = 0; u < NT; ++u) last = last && (u == t || k_done(u, j + 1));
-                  if (last) ptx::mma_commit(&kv_empty[slot_k]);
-                }
-              }
-              if (sd[t]) {
-                const int item_v = kvi + 2 * j + 1, slot_v = item_v % T::STAGES;
-                if (ptx::mbar_test(&p_full[t], pc[t] & 1) &&
-                    ptx::mbar_test(&kv_full[slot_v], (item_v / T::STAGES) & 1)) {
-                  if (itl == 0) FA3B_TP(t, j, 6);
-                  const int buf = pc[t]++ & 1;
-                  ptx::tc_fence_after();
-                  issue_pv_ss(t, slot_v, j > 0, buf);
-                  ptx::mma_commit(&pv_done[2 * t + buf]);
-                  if (j + 1 == w.n_t[t]) ptx::mma_commit(&o_full[t]);
-                  jn[t] = j + 1;
-                  sd[t] = j + 2 >= w.n_t[t];
-                  moved = true;
-                  bool last = true;
-#pragma unroll
-                  for (int u = 0; u < NT; ++u) last = last && (u == t || v_done(u, j));
-                  if (last) ptx::mma_commit(&kv_empty[slot_v]);
-                }
-              }
+          for (int j = 0; j < n; ++j) {
+            const int item_v = kvi + 2 * j + 1, item_k = kvi + 2 * j + 4;
+            ptx::mbar_wait(&kv_full[item_v % T::STAGES], (item_v / T::STAGES) & 1);
+            ptx::mbar_wait(&p_full[0], pc[0]++ & 1);
+            if (itl == 0) FA3B_TP(0, j, 6);
+            ptx::tc_fence_after();
+            issue_pv(0, item_v % T::STAGES, j > 0, T::s2_col((g0 + j) & 1));
+            ptx::mma_commit(pv_done);
+            ptx::mma_commit(&kv_empty[item_v % T::STAGES]);
+            if (j + 1 == n) ptx::mma_commit(&o_full[0]);
+            if (j + 2 < n) {
+              ptx::mbar_wait(&kv_full[item_k % T::STAGES], (item_k / T::STAGES) & 1);
+              ptx::tc_fence_after();
+              s_issue(item_k % T::STAGES);
+              ptx::mma_commit(&kv_empty[item_k % T::STAGES]);
             }
-            if (!left) break;
-            // back off between empty polls: the spinning thread shares its SM
-            // sub-partition's issue slots with two softmax warps
-            if (!moved) __nanosleep(FA3B_MMA_POLL_NS);
           }
           ptx::mma_commit(q_empty);
-          kvi += 2 * w.n_max;
+          kvi += 2 * n;
         }
       } else
       for (int lin = item_of(0); lin < num_items; lin = item_of(++itl)) {
@@ -482,7 +416,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
 #pragma unroll
           for (int t = 0; t < NT; ++t) {
             if (w.n_t[t] == 0) continue;
-            issue_qk(t, slot0);
+            issue_qk(t, slot0, T::s_col(t));
             ptx::mma_commit(&s_full[t]);
           }
           ptx::mma_commit(&kv_empty[slot0]);
@@ -498,14 +432,14 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
             ptx::mbar_wait(&p_full[t], pc[t]++ & 1);
             if (itl == 0) FA3B_TP(t, j, 6);
             ptx::tc_fence_after();
-            issue_pv(t, slot_v, j > 0);
+            issue_pv(t, slot_v, j > 0, T::s_col(t));
             if (j + 1 < w.n_t[t]) {
               if (!k_ready) {
                 ptx::mbar_wait(&kv_full[slot_k], (item_k / T::STAGES) & 1);
                 ptx::tc_fence_after();
                 k_ready = true;
               }
-              issue_qk(t, slot_k);
+              issue_qk(t, slot_k, T::s_col(t));
               ptx::mma_commit(&s_full[t]);
             } else {
               ptx::mma_commit(&o_full[t]);
@@ -526,14 +460,11 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
     const int hh = (warp >> 2) & 1;      // column half of S / O
     const int r = ((warp & 3) << 5) | static_cast<int>(ptx::lane_id());  // row == TMEM lane
     const uint32_t lane_base = static_cast<uint32_t>(32 * (warp & 3)) << 16;
-    const uint32_t tS = tmem + lane_base + T::s_col(t);
+    const uint32_t tS0 = tmem + lane_base + T::s_col(t);
     const uint32_t tO = tmem + lane_base + T::o_col(t);
     float* xch = reinterpret_cast<float*>(smem + T::OFF_XCH) + t * 512;  // [2 buf][2 half][128]
     const uint32_t bar_id = 1 + t;
     int sc = 0, xc = 0, oc = 0;  // s_full / exchange-buffer / o_full uses so far
-    // P_SMEM: P tile #g of this tile goes to buffer g & 1; g = sc - 1 inside an iteration
-    // P_SMEM: this thread's 64 bytes of row r (16B chunks 4 hh .. 4 hh + 3, swizzled)
-    uint8_t* p_row = smem + T::OFF_P + 2 * t * T::P_BYTES + r * 128;
     int itl = 0;
     for (int lin = item_of(0); lin < num_items; lin = item_of(++itl)) {
     const Item w = decode(lin);
@@ -592,8 +523,13 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       }
       const bool tr = itl == 0 && (warp & 7) == 0 && ptx::lane_id() == 0;
       if (tr) FA3B_TP(t, j, 0);
-      ptx::mbar_wait(&s_full[t], sc & 1);
+      if constexpr (T::S2)
+        ptx::mbar_wait(&s_full[(sc & 1) ? NT : 0], (sc >> 1) & 1);
+      else
+        ptx::mbar_wait(&s_full[t], sc & 1);
       ++sc;
+      // S2: S / P of this block live in buffer (sc - 1) & 1
+      const uint32_t tS = T::S2 ? tmem + lane_base + T::s2_col((sc - 1) & 1) : tS0;
       if (tr) FA3B_TP(t, j, 1);
 #ifdef FA3B_TRACE
       if (itl == 0 && j == 0 && threadIdx.x == 0) FA3B_CTA(3, fa3b_gtime());
@@ -616,13 +552,6 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
         }
       };
       load_s();
-      if constexpr (T::P_SMEM) {
-        if (j + 1 < nt) {  // S_t may be overwritten by S(K_{j+1})
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (ptx::lane_id() == 0) ptx::mbar_arrive(&s_free[t]);
-        }
-      }
       if (tr) FA3B_TP(t, j, 2);
       // half-row max: FMNMX3 over 4 independent chains, then swap with the other half
       float a0 = s[0], a1 = s[1], a2 = s[2], a3 = s[3];
@@ -644,7 +573,6 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       constexpr int NPK = FP8 ? 16 : 32;
       uint32_t pk[NPK];
       float psum = 0.f;
-      uint8_t* p_dst = p_row + ((sc - 1) & 1) * T::P_BYTES;  // P_SMEM
       auto exp_half = [&](float msub) {
         const float2 sc2 = make_float2(slj, slj), nm2 = make_float2(lpm - msub, lpm - msub);
         float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
@@ -666,13 +594,6 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
               pk[i >> 1] = ptx::pack_e4m3x4(prev.x, prev.y, pp.x, pp.y);
             else
               prev = pp;
-            if constexpr (T::P_SMEM) {
-              if ((i & 7) == 7) {  // 16 codes = one 16-byte chunk of the swizzled row
-                const int c = i >> 3;
-                *reinterpret_cast<uint4*>(p_dst + (((4 * hh + c) ^ (r & 7)) << 4)) =
-                    make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-              }
-            }
           } else {
             pk[i] = BF16 ? ptx::pack_bf16(pp.x, pp.y) : ptx::pack_f16(pp.x, pp.y);
           }
@@ -687,17 +608,8 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       const bool resc = m_new > m_use + thr;
       const float m_cur = resc ? m_new : m_use;
       const float factor = resc ? ptx::ex2(m_use - m_new) : 1.f;
-      if constexpr (T::P_SMEM) {
-        // P buffer g & 1 (g = sc - 1) is free once PV #(g - 2) (same buffer) has completed
-        if (sc >= 3) ptx::mbar_wait(&pv_done[2 * t + ((sc - 1) & 1)], ((sc - 3) >> 1) & 1);
-      }
       exp_half((m_cur == -INFINITY) ? 0.f : m_cur);
-      if constexpr (T::P_SMEM) {
-        ptx::fence_proxy_async_smem();
-        // O_t may be rescaled once PV #(pg - 1) has completed (the previous item's
-        // last PV was covered by the o_full wait of its epilogue)
-        if (j > 0) ptx::mbar_wait(&pv_done[2 * t + (sc & 1)], ((sc - 2) >> 1) & 1);
-      } else if constexpr (FP8)
+      if constexpr (FP8)
         ptx::tmem_st16(tS + 16 * hh, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
       else
         ptx::tmem_st32(tS + 32 * hh, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
@@ -705,7 +617,8 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       if (tr) FA3B_TP(t, j, 4);
       const float ofac = factor * vfac;
       if (j > 0 && __any_sync(0xffffffffu, ofac != 1.f)) {
-        // PV(V_{j-1}) is complete (see header); rescale this half-row of O_t.
+        // PV(V_{j-1}) is complete (see header; S2: wait for it); rescale this half-row of O_t.
+        if constexpr (T::S2) ptx::mbar_wait(pv_done, (sc - 2) & 1);
         constexpr int G = DH / 32 < 4 ? DH / 32 : 4;
 #pragma unroll
         for (int c0 = 0; c0 < DH / 32; c0 += G) {
