@@ -48,8 +48,8 @@
 // the softmax still works on S_j / P_j — the paper's intra-warpgroup overlap
 // (PAPER.md:307-330). Order S_0 ; S_1 ; { PV_j ; S_{j+2} }_j, S_{j+2} reusing
 // S_j's columns after PV_j has read P_j; pv_done tells the softmax when O may be
-// rescaled. Enabled for e4m3 only: at bf16 d = 256 the two-stage K/V ring
-// (64 KB tiles) cannot feed the earlier K loads (measured slower).
+// rescaled. The producer loads in the same order (K_0, K_1, {V_j, K_{j+2}}), so
+// the two-stage ring of bf16 d = 256 (64 KB tiles) still delivers K_{j+2} early.
 #pragma once
 
 #include "sm100_ptx.cuh"
@@ -150,7 +150,7 @@ struct FwdTraits {
   static constexpr int MMA_WARP = NT * 8 + 1;
   static constexpr uint32_t TMEM_COLS = CPS == 2 ? 256 : 512;
   // one query tile per CTA, e4m3: a second S buffer after O (see the header)
-  static constexpr bool S2 = NT == 1 && CPS == 1 && EB == 1 && FA3B_FWD_S2;
+  static constexpr bool S2 = NT == 1 && CPS == 1 && FA3B_FWD_S2;
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_KV = NT * TILE_BYTES;
   static constexpr int OFF_BAR = OFF_KV + STAGES * TILE_BYTES;
@@ -303,24 +303,38 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
                                ptx::kEvictFirst);
           }
         };
-        // this item's first K/V block streams into the ring while the previous
-        // item's last GEMMs still hold the Q buffer
-        for (int j = 0; j < w.n_max; ++j) {
-          if (j == 1) load_q();
+        auto load_kv = [&](bool is_v, int blk) {
+          const int slot = item % T::STAGES;
+          const uint32_t ph = (item / T::STAGES) & 1;
+          ptx::mbar_wait(&kv_empty[slot], ph ^ 1);
+          ptx::mbar_arrive_expect_tx(&kv_full[slot], T::TILE_BYTES);
+          uint8_t* dst = smem + T::OFF_KV + slot * T::TILE_BYTES;
 #pragma unroll
-          for (int kv = 0; kv < 2; ++kv, ++item) {
-            const int slot = item % T::STAGES;
-            const uint32_t ph = (item / T::STAGES) & 1;
-            ptx::mbar_wait(&kv_empty[slot], ph ^ 1);
-            ptx::mbar_arrive_expect_tx(&kv_full[slot], T::TILE_BYTES);
-            uint8_t* dst = smem + T::OFF_KV + slot * T::TILE_BYTES;
-#pragma unroll
-            for (int c = 0; c < T::CHUNKS; ++c)
-              ptx::tma_load_4d(dst + c * T::CHUNK_BYTES, kv ? &tmV : &tmK, &kv_full[slot],
-                               c * T::CHUNK_ELEMS, w.hkv, j * 128, w.b, ptx::kEvictLast);
+          for (int c = 0; c < T::CHUNKS; ++c)
+            ptx::tma_load_4d(dst + c * T::CHUNK_BYTES, is_v ? &tmV : &tmK, &kv_full[slot],
+                             c * T::CHUNK_ELEMS, w.hkv, blk * 128, w.b, ptx::kEvictLast);
+          ++item;
+        };
+        if constexpr (T::S2) {
+          // the MMA warp's order: K_0, K_1, { V_j, K_{j+2} }_j
+          const int n = w.n_t[0];
+          load_kv(false, 0);
+          if (n > 1) load_kv(false, 1);
+          load_q();
+          for (int j = 0; j < n; ++j) {
+            load_kv(true, j);
+            if (j + 2 < n) load_kv(false, j + 2);
           }
+        } else {
+          // this item's first K/V block streams into the ring while the previous
+          // item's last GEMMs still hold the Q buffer
+          for (int j = 0; j < w.n_max; ++j) {
+            if (j == 1) load_q();
+            load_kv(false, j);
+            load_kv(true, j);
+          }
+          if (w.n_max == 1) load_q();
         }
-        if (w.n_max == 1) load_q();
       }
     }
   } else if (warp == T::MMA_WARP) {
@@ -378,28 +392,30 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
           const int n = w.n_t[0];
           ptx::mbar_wait(q_full, itl & 1);
           const int g0 = gs;  // global index of this item's S_0
-          for (int j = 0; j < 2 && j < n; ++j) {
-            const int item_k = kvi + 2 * j;
-            ptx::mbar_wait(&kv_full[item_k % T::STAGES], (item_k / T::STAGES) & 1);
+          int pos = kvi;      // ring position, in the producer's order K_0, K_1, {V_j, K_{j+2}}
+          auto wait_pos = [&]() {
+            ptx::mbar_wait(&kv_full[pos % T::STAGES], (pos / T::STAGES) & 1);
             ptx::tc_fence_after();
-            s_issue(item_k % T::STAGES);
-            ptx::mma_commit(&kv_empty[item_k % T::STAGES]);
+            return pos++ % T::STAGES;
+          };
+          for (int j = 0; j < 2 && j < n; ++j) {
+            const int slot = wait_pos();
+            s_issue(slot);
+            ptx::mma_commit(&kv_empty[slot]);
           }
           for (int j = 0; j < n; ++j) {
-            const int item_v = kvi + 2 * j + 1, item_k = kvi + 2 * j + 4;
-            ptx::mbar_wait(&kv_full[item_v % T::STAGES], (item_v / T::STAGES) & 1);
+            const int slot_v = wait_pos();
             ptx::mbar_wait(&p_full[0], pc[0]++ & 1);
             if (itl == 0) FA3B_TP(0, j, 6);
             ptx::tc_fence_after();
-            issue_pv(0, item_v % T::STAGES, j > 0, T::s2_col((g0 + j) & 1));
+            issue_pv(0, slot_v, j > 0, T::s2_col((g0 + j) & 1));
             ptx::mma_commit(pv_done);
-            ptx::mma_commit(&kv_empty[item_v % T::STAGES]);
+            ptx::mma_commit(&kv_empty[slot_v]);
             if (j + 1 == n) ptx::mma_commit(&o_full[0]);
             if (j + 2 < n) {
-              ptx::mbar_wait(&kv_full[item_k % T::STAGES], (item_k / T::STAGES) & 1);
-              ptx::tc_fence_after();
-              s_issue(item_k % T::STAGES);
-              ptx::mma_commit(&kv_empty[item_k % T::STAGES]);
+              const int slot_k = wait_pos();
+              s_issue(slot_k);
+              ptx::mma_commit(&kv_empty[slot_k]);
             }
           }
           ptx::mma_commit(q_empty);
@@ -616,9 +632,13 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       l = l * factor + psum * inv_pmul;
       if (tr) FA3B_TP(t, j, 4);
       const float ofac = factor * vfac;
+      // S2: every iteration waits for PV(V_{j-1}) before handing over P_j, so one
+      // PV is in flight at a time and the pv_done parity never skips a phase (a
+      // wait only when O needs rescaling hung at bf16 d = 256)
+      if constexpr (T::S2)
+        if (j > 0) ptx::mbar_wait(pv_done, (sc - 2) & 1);
       if (j > 0 && __any_sync(0xffffffffu, ofac != 1.f)) {
-        // PV(V_{j-1}) is complete (see header; S2: wait for it); rescale this half-row of O_t.
-        if constexpr (T::S2) ptx::mbar_wait(pv_done, (sc - 2) & 1);
+        // PV(V_{j-1}) is complete (see header / above); rescale this half-row of O_t.
         constexpr int G = DH / 32 < 4 ? DH / 32 : 4;
 #pragma unroll
         for (int c0 = 0; c0 < DH / 32; c0 += G) {

@@ -13,7 +13,13 @@
 #include <cuda_fp16.h>
 #include <cuda_fp8.h>
 #include <stdint.h>
+#ifdef FA3B_WATCHDOG_PRINT
+#include <cstdio>
+#endif
 
+#ifndef FA3B_WATCHDOG_LOG2
+#define FA3B_WATCHDOG_LOG2 34
+#endif
 #ifndef FA3B_WATCHDOG
 #define FA3B_WATCHDOG 1
 #endif
@@ -89,7 +95,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #if FA3B_WATCHDOG
   const long long t0 = clock64();
   while (!mbar_try_wait(a, parity)) {
-    if (clock64() - t0 > (1ll << 34)) __trap();
+    if (clock64() - t0 > (1ll << FA3B_WATCHDOG_LOG2)) {
+#ifdef FA3B_WATCHDOG_PRINT
+      printf("fa3b watchdog: block %d thread %d smem bar 0x%x parity %u\n", blockIdx.x, threadIdx.x, a, parity);
+#endif
+      __trap();
+    }
   }
 #else
   while (!mbar_try_wait(a, parity)) {
