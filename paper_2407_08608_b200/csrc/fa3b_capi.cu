@@ -156,10 +156,16 @@ int validate_problem(int batch, int heads_q, int heads_kv, int seqlen, int head_
 
 namespace {
 
+#ifndef FA3B_FWD_EMU_S2_16
+#define FA3B_FWD_EMU_S2_16 2
+#endif
+
 template <int D, int NT, bool CAUSAL, bool BF16, int CPS>
 int launch_fwd16(const fa3b_fwd_params& p, cudaStream_t stream) {
   using T = FwdTraits<D, NT, 2, CPS>;
-  auto kern = fa3b_fwd_kernel<D, NT, CAUSAL, BF16 ? KIND_BF16 : KIND_F16, CPS>;
+  // one-tile CTAs (S2) own the SM's MUFU: FA3B_FWD_EMU_S2_16 of every 8 exp2 pairs on FMA
+  constexpr int EMU = T::S2 ? FA3B_FWD_EMU_S2_16 : FA3B_FWD_EMU;
+  auto kern = fa3b_fwd_kernel<D, NT, CAUSAL, BF16 ? KIND_BF16 : KIND_F16, CPS, EMU>;
   int rc = ensure_smem_attr(reinterpret_cast<const void*>(kern), T::SMEM_BYTES);
   if (rc != FA3B_OK) return rc;
 
