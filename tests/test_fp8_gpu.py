@@ -139,3 +139,48 @@ def test_fp8_rejects_bad_blocks(cuda):
         api.fwd(q8, q8, q8, q_scale=s, k_scale=s, v_scale=s, q_block_rows=64, kv_block_rows=64)
     with pytest.raises(Fa3bError, match="power of two"):
         api.fp8_prepare(torch.randn(1, 8, 1, 96, device="cuda"))
+
+
+@pytest.mark.parametrize("B,N,H,D,causal,per_block", [(1, 16384, 8, 256, False, True),
+                                                      (2, 4173, 8, 256, True, True),
+                                                      (1, 16384, 8, 256, False, False)])
+def test_fp8_one_tile_many_items(cuda, B, N, H, D, causal, per_block):
+    """K6 at d256 runs one query tile per CTA with a second S buffer in TMEM: many work
+    items per persistent CTA, ragged causal blocks, both scale granularities (no
+    Hadamard, so torch can emulate the quantization). Sampled rows against fp32 torch;
+    yardstick: the same attention on e4m3-rounded Q/K/V (128-row block or tensor
+    scales) and e4m3 P (scale 1/448), error within 1.3x of that emulation's."""
+    from paper_2407_08608_b200 import api
+    import torch
+    e4m3 = torch.float8_e4m3fn
+    gen = torch.Generator(device="cuda").manual_seed(N + H)
+    q, k, v = (torch.randn(B, N, H, D, device="cuda", generator=gen, dtype=torch.bfloat16)
+               for _ in range(3))
+    o, lse = api.fp8_fwd(q, k, v, causal=causal, per_block=per_block, incoherent=False,
+                         out_dtype=torch.float32)
+
+    def quant(x):  # [N, D] fp32 -> e4m3-rounded values with the kernel's scales
+        nb = (N + 127) // 128
+        xp = torch.zeros(nb * 128, D, device="cuda")
+        xp[:N] = x
+        xb = xp.view(nb, 128, D) if per_block else xp.view(1, -1, D)
+        sc = xb.abs().amax(dim=(1, 2), keepdim=True) / 448
+        return ((xb / sc).to(e4m3).float() * sc).view(-1, D)[:N]
+
+    rows = torch.unique(torch.cat([torch.tensor([0, 127, 128, N - 1]),
+                                   torch.randint(0, N, (60,), generator=gen, device="cuda").cpu()])).cuda()
+    alpha = 1 / math.sqrt(D)
+    for b in sorted({0, B - 1}):
+        for h in (0, H - 1):
+            qf, kf, vf = (x[b, :, h].float() for x in (q, k, v))
+            mask = torch.arange(N, device="cuda")[None, :] > rows[:, None]
+            s = alpha * qf[rows] @ kf.T
+            s8 = alpha * quant(qf)[rows] @ quant(kf).T
+            if causal:
+                s, s8 = s.masked_fill(mask, -math.inf), s8.masked_fill(mask, -math.inf)
+            ref = torch.softmax(s, -1) @ vf
+            p = torch.exp(s8 - s8.amax(-1, keepdim=True))
+            emu = ((p * 448).to(e4m3).float() / 448) @ quant(vf) / p.sum(-1, keepdim=True)
+            err, err_emu = (o[b, rows, h] - ref).norm().item(), (emu - ref).norm().item()
+            assert err <= 1.3 * err_emu + 1e-3 * ref.norm().item(), (err, err_emu)
+            assert (lse[b, h, rows] - torch.logsumexp(s, -1)).abs().max().item() < 0.05

@@ -214,3 +214,34 @@ def test_fwd_rejects_bad_arguments(cuda):
     q = torch.zeros(1, 128, 2, 64, device="cuda", dtype=torch.bfloat16)
     with pytest.raises(Fa3bError, match="alpha"):
         api.fwd(q, q, q, alpha=0.0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("B,N,H,Hkv,D,causal,sched", [
+    (1, 16384, 8, 8, 256, False, "pingpong"),   # 1024 items: ~7 per CTA (the S2 hang case)
+    (2, 4173, 8, 2, 256, True, "pingpong"),     # ragged causal GQA, one-tile S2 path
+    (1, 16384, 16, 16, 128, True, "basic"),     # one-tile S2 at d128, causal
+    (3, 1000, 32, 8, 64, False, "basic"),       # one-tile S2 at d64, ragged
+])
+def test_one_tile_double_buffered_s(cuda, B, N, H, Hkv, D, causal, sched):
+    """One-tile CTAs keep two S buffers in TMEM and load K/V in MMA order (K_0, K_1,
+    {V_j, K_{j+2}}); many work items per persistent CTA, ragged and causal blocks,
+    GQA: sampled rows of every checked head against fp32 torch."""
+    api = _api()
+    torch = _torch()
+    gen = torch.Generator(device="cuda").manual_seed(N + D)
+    q = torch.randn(B, N, H, D, device="cuda", generator=gen, dtype=torch.bfloat16)
+    k, v = (torch.randn(B, N, Hkv, D, device="cuda", generator=gen, dtype=torch.bfloat16)
+            for _ in range(2))
+    o, lse = api.fwd(q, k, v, causal=causal, schedule=sched)
+    alpha = 1 / math.sqrt(D)
+    rows = torch.unique(torch.cat([torch.tensor([0, 127, 128, N - 1]),
+                                   torch.randint(0, N, (60,), generator=gen, device="cuda").cpu()])).cuda()
+    for b in sorted({0, B - 1}):
+        for h in sorted({0, H // 3, H - 1}):
+            kh = h // (H // Hkv)
+            s = alpha * q[b, rows, h].float() @ k[b, :, kh].float().T
+            if causal:
+                s = s.masked_fill(torch.arange(N, device="cuda")[None, :] > rows[:, None], -math.inf)
+            assert (o[b, rows, h].float() - torch.softmax(s, -1) @ v[b, :, kh].float()).abs().max().item() < 2e-2
+            assert (lse[b, h, rows] - torch.logsumexp(s, -1)).abs().max().item() < 1e-3
