@@ -50,6 +50,12 @@
 // S_j's columns after PV_j has read P_j; pv_done tells the softmax when O may be
 // rescaled. The producer loads in the same order (K_0, K_1, {V_j, K_{j+2}}), so
 // the two-stage ring of bf16 d = 256 (64 KB tiles) still delivers K_{j+2} early.
+//
+// The d = 64 tile pair (T::S3) has 128 spare columns too: three S buffers rotate
+// between the two tiles, S(t, j) in buffer (G + 2 j + t) % 3, in the order
+// S(0,0) ; S(1,0) ; S(0,1) ; {PV(0,j) ; S(1,j+1) ; PV(1,j) ; S(0,j+2)}_j — every S
+// reuses the buffer of the S three before it, whose PV was issued just before, and
+// each tile's next S is computed during its own softmax.
 #pragma once
 
 #include "sm100_ptx.cuh"
@@ -62,6 +68,9 @@
 #endif
 #ifndef FA3B_FWD_S2
 #define FA3B_FWD_S2 1
+#endif
+#ifndef FA3B_FWD_S3
+#define FA3B_FWD_S3 1
 #endif
 #ifndef FA3B_FWD_OREGS
 #define FA3B_FWD_OREGS 56
@@ -151,12 +160,15 @@ struct FwdTraits {
   static constexpr uint32_t TMEM_COLS = CPS == 2 ? 256 : 512;
   // one query tile per CTA, e4m3: a second S buffer after O (see the header)
   static constexpr bool S2 = NT == 1 && CPS == 1 && FA3B_FWD_S2;
+  // d = 64 tile pair: three S buffers rotate between the two tiles (3 x 128 + 2 x 64
+  // columns), so each tile's next S is computed during its softmax (see the header)
+  static constexpr bool S3 = NT == 2 && D == 64 && CPS == 1 && FA3B_FWD_S3;
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_KV = NT * TILE_BYTES;
   static constexpr int OFF_BAR = OFF_KV + STAGES * TILE_BYTES;
-  // q_full, kv_full[S], kv_empty[S], s_full[NT + 1], p_full[NT], o_full[NT], q_empty,
-  // pv_done (s_full[NT] and pv_done serve S2)
-  static constexpr int NUM_BARS = 4 + 2 * STAGES + 3 * NT;
+  // q_full, kv_full[S], kv_empty[S], s_full[2 NT], p_full[NT], o_full[NT], q_empty,
+  // pv_done[NT] (the second s_full per tile and pv_done serve S2 / S3)
+  static constexpr int NUM_BARS = 3 + 2 * STAGES + 5 * NT;
   // row-max / row-sum exchange between the two column halves: [NT][2 buf][2 half][128]
   static constexpr int OFF_XCH = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr int SMEM_BYTES = OFF_XCH + NT * 2 * 2 * 128 * 4 + 1024;
@@ -165,7 +177,7 @@ struct FwdTraits {
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
   __host__ __device__ static constexpr int s_col(int t) { return t * 128; }
   __host__ __device__ static constexpr int s2_col(int buf) { return buf ? 128 + D : 0; }
-  __host__ __device__ static constexpr int o_col(int t) { return NT * 128 + t * D; }
+  __host__ __device__ static constexpr int o_col(int t) { return (S3 ? 384 : NT * 128) + t * D; }
 };
 
 // EMU: how many of every 8 exp2 pairs run on the FMA-pipe polynomial.
@@ -190,10 +202,10 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
   uint64_t* kv_full = bars + 1;
   uint64_t* kv_empty = kv_full + T::STAGES;
   uint64_t* s_full = kv_empty + T::STAGES;
-  uint64_t* p_full = s_full + NT + 1;  // (s_full[NT] is the S2 second buffer's)
+  uint64_t* p_full = s_full + 2 * NT;  // S2 / S3: s_full[2 t + (S count of tile t & 1)]
   uint64_t* o_full = p_full + NT;
   uint64_t* q_empty = o_full + NT;  // the Q tiles of a work item are consumed
-  uint64_t* pv_done = q_empty + 1;  // S2: PV complete
+  uint64_t* pv_done = q_empty + 1;  // S2 / S3: [t] PV of tile t complete
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + T::NUM_BARS);
 
   const int warp = static_cast<int>(ptx::warp_id());
@@ -251,13 +263,13 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
         ptx::mbar_init(&kv_empty[s], 1);
       }
       for (int t = 0; t < NT; ++t) {
-        ptx::mbar_init(&s_full[t], 1);
-        if (t == 0) ptx::mbar_init(&s_full[NT], 1);
+        ptx::mbar_init(&s_full[2 * t], 1);
+        ptx::mbar_init(&s_full[2 * t + 1], 1);
+        ptx::mbar_init(&pv_done[t], 1);
         ptx::mbar_init(&p_full[t], 8);  // one arrival per softmax warp
         ptx::mbar_init(&o_full[t], 1);
       }
       ptx::mbar_init(q_empty, 1);
-      ptx::mbar_init(pv_done, 1);
       ptx::fence_mbar_init();
     }
     __syncwarp();
@@ -315,9 +327,9 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
                              c * T::CHUNK_ELEMS, w.hkv, blk * 128, w.b, ptx::kEvictLast);
           ++item;
         };
-        if constexpr (T::S2) {
+        if constexpr (T::S2 || T::S3) {
           // the MMA warp's order: K_0, K_1, { V_j, K_{j+2} }_j
-          const int n = w.n_t[0];
+          const int n = w.n_max;
           load_kv(false, 0);
           if (n > 1) load_kv(false, 1);
           load_q();
@@ -384,7 +396,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
         int gs = 0;  // S GEMMs issued so far
         auto s_issue = [&](int slot) {
           issue_qk(0, slot, T::s2_col(gs & 1));
-          ptx::mma_commit(&s_full[(gs & 1) ? NT : 0]);
+          ptx::mma_commit(&s_full[gs & 1]);
           ++gs;
         };
         for (int lin = item_of(0); lin < num_items; lin = item_of(++itl)) {
@@ -409,7 +421,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
             if (itl == 0) FA3B_TP(0, j, 6);
             ptx::tc_fence_after();
             issue_pv(0, slot_v, j > 0, T::s2_col((g0 + j) & 1));
-            ptx::mma_commit(pv_done);
+            ptx::mma_commit(&pv_done[0]);
             ptx::mma_commit(&kv_empty[slot_v]);
             if (j + 1 == n) ptx::mma_commit(&o_full[0]);
             if (j + 2 < n) {
@@ -420,6 +432,73 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
           }
           ptx::mma_commit(q_empty);
           kvi += 2 * n;
+        }
+      } else if constexpr (T::S3) {
+        // Two tiles, three S buffers: S(t, j) -> buffer (G + 2 j + t) % 3 with G the
+        // item base. Per item: S(0,0) ; S(1,0) ; S(0,1) ;
+        //   { PV(0,j) ; S(1,j+1) ; PV(1,j) ; S(0,j+2) }_j
+        // Each S reuses the buffer of S number g - 3, whose PV was issued just before.
+        int gb = 0;        // G of this item
+        int sn[NT] = {};   // S GEMMs issued per tile (s_full parity)
+        auto s_issue = [&](int t, int j, int slot) {
+          issue_qk(t, slot, 128 * ((gb + 2 * j + t) % 3));
+          ptx::mma_commit(&s_full[2 * t + (sn[t] & 1)]);
+          ++sn[t];
+        };
+        for (int lin = item_of(0); lin < num_items; lin = item_of(++itl)) {
+          const Item w = decode(lin);
+          const int n0 = w.n_t[0], n1 = w.n_t[1], n = w.n_max;
+          // the last reader of K_j / V_j releases its ring slot
+          auto last_t = [&](int j) { return j < n1 ? 1 : 0; };
+          ptx::mbar_wait(q_full, itl & 1);
+          int pos = kvi;  // ring position, producer order K_0, K_1, {V_j, K_{j+2}}
+          auto wait_pos = [&]() {
+            ptx::mbar_wait(&kv_full[pos % T::STAGES], (pos / T::STAGES) & 1);
+            ptx::tc_fence_after();
+            return pos++ % T::STAGES;
+          };
+          const int k0 = wait_pos();
+          if (n0 > 0) s_issue(0, 0, k0);
+          if (n1 > 0) s_issue(1, 0, k0);
+          ptx::mma_commit(&kv_empty[k0]);
+          int k1 = -1;  // K_1's slot, released by S(1,1)
+          if (n > 1) {
+            k1 = wait_pos();
+            if (n0 > 1) s_issue(0, 1, k1);
+            if (last_t(1) == 0) ptx::mma_commit(&kv_empty[k1]);
+          }
+          int kn = k1;  // slot of K_{j+1}
+          for (int j = 0; j < n; ++j) {
+            const int slot_v = wait_pos();
+            if (j < n0) {
+              ptx::mbar_wait(&p_full[0], pc[0]++ & 1);
+              ptx::tc_fence_after();
+              issue_pv(0, slot_v, j > 0, 128 * ((gb + 2 * j) % 3));
+              ptx::mma_commit(&pv_done[0]);
+              if (j + 1 == n0) ptx::mma_commit(&o_full[0]);
+              if (last_t(j) == 0) ptx::mma_commit(&kv_empty[slot_v]);
+            }
+            if (j + 1 < n1) {
+              s_issue(1, j + 1, kn);
+              ptx::mma_commit(&kv_empty[kn]);
+            }
+            if (j < n1) {
+              ptx::mbar_wait(&p_full[1], pc[1]++ & 1);
+              ptx::tc_fence_after();
+              issue_pv(1, slot_v, j > 0, 128 * ((gb + 2 * j + 1) % 3));
+              ptx::mma_commit(&pv_done[1]);
+              if (j + 1 == n1) ptx::mma_commit(&o_full[1]);
+              ptx::mma_commit(&kv_empty[slot_v]);
+            }
+            if (j + 2 < n) {
+              kn = wait_pos();
+              if (j + 2 < n0) s_issue(0, j + 2, kn);
+              if (last_t(j + 2) == 0) ptx::mma_commit(&kv_empty[kn]);
+            }
+          }
+          ptx::mma_commit(q_empty);
+          kvi += 2 * n;
+          gb += 2 * n;
         }
       } else
       for (int lin = item_of(0); lin < num_items; lin = item_of(++itl)) {
@@ -433,7 +512,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
           for (int t = 0; t < NT; ++t) {
             if (w.n_t[t] == 0) continue;
             issue_qk(t, slot0, T::s_col(t));
-            ptx::mma_commit(&s_full[t]);
+            ptx::mma_commit(&s_full[2 * t]);
           }
           ptx::mma_commit(&kv_empty[slot0]);
         }
@@ -456,7 +535,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
                 k_ready = true;
               }
               issue_qk(t, slot_k, T::s_col(t));
-              ptx::mma_commit(&s_full[t]);
+              ptx::mma_commit(&s_full[2 * t]);
             } else {
               ptx::mma_commit(&o_full[t]);
             }
@@ -481,6 +560,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
     float* xch = reinterpret_cast<float*>(smem + T::OFF_XCH) + t * 512;  // [2 buf][2 half][128]
     const uint32_t bar_id = 1 + t;
     int sc = 0, xc = 0, oc = 0;  // s_full / exchange-buffer / o_full uses so far
+    int gbase = 0;               // S3: 2 x (KV blocks of this CTA's previous items)
     int itl = 0;
     for (int lin = item_of(0); lin < num_items; lin = item_of(++itl)) {
     const Item w = decode(lin);
@@ -539,13 +619,16 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       }
       const bool tr = itl == 0 && (warp & 7) == 0 && ptx::lane_id() == 0;
       if (tr) FA3B_TP(t, j, 0);
-      if constexpr (T::S2)
-        ptx::mbar_wait(&s_full[(sc & 1) ? NT : 0], (sc >> 1) & 1);
+      if constexpr (T::S2 || T::S3)
+        ptx::mbar_wait(&s_full[2 * t + (sc & 1)], (sc >> 1) & 1);
       else
-        ptx::mbar_wait(&s_full[t], sc & 1);
+        ptx::mbar_wait(&s_full[2 * t], sc & 1);
       ++sc;
       // S2: S / P of this block live in buffer (sc - 1) & 1
-      const uint32_t tS = T::S2 ? tmem + lane_base + T::s2_col((sc - 1) & 1) : tS0;
+      // S3: S(t, j) lives in buffer (item base + 2 j + t) % 3
+      const uint32_t tS = T::S2   ? tmem + lane_base + T::s2_col((sc - 1) & 1)
+                          : T::S3 ? tmem + lane_base + 128 * ((gbase + 2 * j + t) % 3)
+                                  : tS0;
       if (tr) FA3B_TP(t, j, 1);
 #ifdef FA3B_TRACE
       if (itl == 0 && j == 0 && threadIdx.x == 0) FA3B_CTA(3, fa3b_gtime());
@@ -635,8 +718,8 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       // S2: every iteration waits for PV(V_{j-1}) before handing over P_j, so one
       // PV is in flight at a time and the pv_done parity never skips a phase (a
       // wait only when O needs rescaling hung at bf16 d = 256)
-      if constexpr (T::S2)
-        if (j > 0) ptx::mbar_wait(pv_done, (sc - 2) & 1);
+      if constexpr (T::S2 || T::S3)
+        if (j > 0) ptx::mbar_wait(&pv_done[t], (sc - 2) & 1);
       if (j > 0 && __any_sync(0xffffffffu, ofac != 1.f)) {
         // PV(V_{j-1}) is complete (see header / above); rescale this half-row of O_t.
         constexpr int G = DH / 32 < 4 ? DH / 32 : 4;
@@ -711,6 +794,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
         args.lse[(static_cast<size_t>(b) * args.H + h) * N + q_row] = lse;
       }
     }
+    gbase += 2 * w.n_max;
     }  // work items
   }
 
