@@ -191,44 +191,99 @@ __device__ __forceinline__ void quad_store(const PrepArgs& a, int b, int h, int 
 
 // 128-row blocks, d = 64 / 128: the 16 warps of quad-layout rows hold the whole
 // transformed block in registers across the amax (one read of the input).
-template <int D>
-__global__ void __launch_bounds__(512) fa3b_fp8_prepare_quad_kernel(const PrepArgs a) {
+// Persistent (one CTA per SM walking (block, head, batch) items) with the next
+// item's rows streaming into shared memory by cp.async while the current one is
+// transformed: a CTA needs all 120 registers of 512 threads, so without the
+// prefetch every block's load latency sat exposed in front of its FP64 work.
+template <int D, int ESZ>
+__global__ void __launch_bounds__(512, 1) fa3b_fp8_prepare_quad_kernel(const PrepArgs a, int items) {
   using QD = Quad<D>;
-  const int blk = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  constexpr int Q = QD::Q;
+  constexpr int NV = Q * ESZ / 16;  // 16-byte vectors per thread and block
+  extern __shared__ uint4 stage[];  // [2 stages][NV][512 threads]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, qd = lane % QD::LPR;
-  const int row = blk * 128 + warp * QD::RPW + lane / QD::LPR;
-  const bool valid = row < a.N;
-  __shared__ double s_amax[16];
-  __shared__ int s_bad[16];
-  double v[QD::Q];
-  quad_load<D>(a, b, h, row, valid, qd, v);
-  quad_transform<D>(a, qd, v);
-  double amax = 0.0;
-  bool bad = false;
+  const int rloc = warp * QD::RPW + lane / QD::LPR;
+  __shared__ double s_amax[2][16];
+  __shared__ int s_bad[2][16];
+  auto coords = [&](int item, int& blk, int& h, int& b) {
+    blk = item % a.nblk;
+    const int hb = item / a.nblk;
+    h = hb % a.H;
+    b = hb / a.H;
+  };
+  auto prefetch = [&](int item, int st) {
+    if (item < items) {
+      int blk, h, b;
+      coords(item, blk, h, b);
+      const int row = blk * 128 + rloc;
+      const bool valid = row < a.N;
+      const char* src = static_cast<const char*>(a.src) +
+                        (b * a.s_sb + static_cast<long long>(valid ? row : 0) * a.s_ss + h * a.s_sh + qd * Q) * ESZ;
 #pragma unroll
-  for (int e = 0; e < QD::Q; ++e) {
-    const double x = fabs(v[e]);
-    bad |= !isfinite(x);
-    amax = fmax(amax, x);
-  }
+      for (int k = 0; k < NV; ++k) {
+        const uint32_t dst = ptx::smem_u32(&stage[(st * NV + k) * 512 + threadIdx.x]);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src + 16 * k),
+                     "r"(valid ? 16 : 0)
+                     : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  int st = 0;
+  prefetch(blockIdx.x, 0);
+  for (int item = blockIdx.x, it = 0; item < items; item += gridDim.x, ++it, st ^= 1) {
+    prefetch(item + gridDim.x, st ^ 1);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    int blk, h, b;
+    coords(item, blk, h, b);
+    const int row = blk * 128 + rloc;
+    double v[Q];
+    {
+      uint4 raw[NV];
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, off));
-  bad = __any_sync(0xffffffffu, bad);
-  if (lane == 0) {
-    s_amax[warp] = amax;
-    s_bad[warp] = bad;
-  }
-  __syncthreads();
-  amax = s_amax[0];
-  bad = s_bad[0];
+      for (int k = 0; k < NV; ++k) raw[k] = stage[(st * NV + k) * 512 + threadIdx.x];
+      const uint32_t* u = reinterpret_cast<const uint32_t*>(raw);
 #pragma unroll
-  for (int w = 1; w < 16; ++w) {
-    amax = fmax(amax, s_amax[w]);
-    bad |= s_bad[w] != 0;
+      for (int e = 0; e < Q; ++e) {
+        if constexpr (ESZ == 4) {
+          v[e] = __uint_as_float(u[e]);
+        } else {
+          const uint16_t bits = static_cast<uint16_t>(u[e >> 1] >> (16 * (e & 1)));
+          v[e] = a.src_dtype == FA3B_DTYPE_BF16 ? __uint_as_float(static_cast<uint32_t>(bits) << 16)
+                                                : __half2float(__ushort_as_half(bits));
+        }
+      }
+    }
+    quad_transform<D>(a, qd, v);
+    double amax = 0.0;
+    bool bad = false;
+#pragma unroll
+    for (int e = 0; e < Q; ++e) {
+      const double x = fabs(v[e]);
+      bad |= !isfinite(x);
+      amax = fmax(amax, x);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+    bad = __any_sync(0xffffffffu, bad);
+    const int sb = it & 1;  // two reduction buffers: the next item's writes cannot race these reads
+    if (lane == 0) {
+      s_amax[sb][warp] = amax;
+      s_bad[sb][warp] = bad;
+    }
+    __syncthreads();
+    amax = s_amax[sb][0];
+    bad = s_bad[sb][0];
+#pragma unroll
+    for (int w = 1; w < 16; ++w) {
+      amax = fmax(amax, s_amax[sb][w]);
+      bad |= s_bad[sb][w] != 0;
+    }
+    if (threadIdx.x == 0) write_scale(a, b, h, blk, amax, bad);
+    const double inv = 1.0 / (amax == 0.0 ? 1.0 : amax / 448.0);  // quantize.cpp:25
+    if (row < a.N) quad_store<D>(a, b, h, row, qd, v, inv);
   }
-  if (threadIdx.x == 0) write_scale(a, b, h, blk, amax, bad);
-  const double inv = 1.0 / (amax == 0.0 ? 1.0 : amax / 448.0);  // quantize.cpp:25
-  if (valid) quad_store<D>(a, b, h, row, qd, v, inv);
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -403,10 +458,21 @@ extern "C" int fa3b_fp8_prepare(const fa3b_fp8_prepare_params* pp) {
   cudaError_t e = cudaSuccess;
   if (p.block_rows == 128 && p.head_dim <= 128) {
     // d = 256 would hold 64 doubles per thread; it takes the two-pass kernel instead
-    if (p.head_dim == 64)
-      fa3b_fp8_prepare_quad_kernel<64><<<grid, 512, 0, st>>>(a);
-    else
-      fa3b_fp8_prepare_quad_kernel<128><<<grid, 512, 0, st>>>(a);
+    const int items = a.nblk * p.heads * p.batch;
+    // persistent at d = 128 (+7 %); d = 64 (half the FP64 work per block) was faster
+    // with one CTA per item (1334 vs 1073 GB/s), where the prefetch is a no-op
+    const int pgrid = (p.head_dim == 64 || items < num_sms()) ? items : num_sms();
+    const bool f32 = p.src_dtype == FA3B_DTYPE_F32;
+    const int smem = 2 * 512 * (p.head_dim / 4) * (f32 ? 4 : 2);
+    auto go = [&](auto kern) {
+      const int rc = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
+      if (rc == FA3B_OK) kern<<<pgrid, 512, smem, st>>>(a, items);
+      return rc;
+    };
+    const int rc = p.head_dim == 64
+                       ? (f32 ? go(fa3b_fp8_prepare_quad_kernel<64, 4>) : go(fa3b_fp8_prepare_quad_kernel<64, 2>))
+                       : (f32 ? go(fa3b_fp8_prepare_quad_kernel<128, 4>) : go(fa3b_fp8_prepare_quad_kernel<128, 2>));
+    if (rc != FA3B_OK) return rc;
   } else {
     switch (p.head_dim) {
       case 64: e = launch_generic<64>(a, grid, st); break;
