@@ -180,6 +180,9 @@ struct BwdTraits {
   static constexpr int SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr int COL_S = 0, COL_DP = 128, COL_DV = 256, COL_DK = 256 + D;
   static constexpr int COL_DQ = DQ_IN_DP ? COL_DP : 256 + 2 * D;
+#ifndef FA3B_BWD_EMU64
+#define FA3B_BWD_EMU64 2
+#endif
 #ifndef FA3B_BWD_EMU128
 #define FA3B_BWD_EMU128 0
 #endif
@@ -187,7 +190,7 @@ struct BwdTraits {
 #define FA3B_BWD_S_EARLY 1
 #endif
   // exp2 pairs (of every 8) evaluated on the FMA-pipe polynomial instead of MUFU.EX2
-  static constexpr int EMU = D == 64 ? 2 : FA3B_BWD_EMU128;
+  static constexpr int EMU = D == 64 ? FA3B_BWD_EMU64 : FA3B_BWD_EMU128;
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 };
 

@@ -245,3 +245,26 @@ def test_one_tile_double_buffered_s(cuda, B, N, H, Hkv, D, causal, sched):
                 s = s.masked_fill(torch.arange(N, device="cuda")[None, :] > rows[:, None], -math.inf)
             assert (o[b, rows, h].float() - torch.softmax(s, -1) @ v[b, :, kh].float()).abs().max().item() < 2e-2
             assert (lse[b, h, rows] - torch.logsumexp(s, -1)).abs().max().item() < 1e-3
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("D", [64, 256])
+@pytest.mark.parametrize("causal", [False, True])
+def test_tiny_and_ragged_lengths_buffer_rotation(cuda, D, causal):
+    """The S-buffer schedules (three rotating buffers at d64, two at d256) at every
+    block-count edge: N = 1, partial first block, exactly one / two blocks, one past.
+    All heads and rows against fp32 torch."""
+    api = _api()
+    torch = _torch()
+    for N in (1, 5, 127, 128, 129, 255, 256, 257, 383, 640):
+        gen = torch.Generator(device="cuda").manual_seed(N * 7 + D)
+        B, H = 2, 3
+        q, k, v = (torch.randn(B, N, H, D, device="cuda", generator=gen, dtype=torch.bfloat16)
+                   for _ in range(3))
+        o, lse = api.fwd(q, k, v, causal=causal)
+        s = (q.float().permute(0, 2, 1, 3) @ k.float().permute(0, 2, 3, 1)) / math.sqrt(D)
+        if causal:
+            s = s.masked_fill(torch.ones(N, N, device="cuda", dtype=torch.bool).triu(1), -math.inf)
+        ref = (torch.softmax(s, -1) @ v.float().permute(0, 2, 1, 3)).permute(0, 2, 1, 3)
+        assert (o.float() - ref).abs().max().item() < 2e-2, N
+        assert (lse - torch.logsumexp(s, -1)).abs().max().item() < 1e-3, N
