@@ -158,11 +158,13 @@ struct FwdTraits {
   static constexpr int LOAD_WARP = NT * 8;
   static constexpr int MMA_WARP = NT * 8 + 1;
   static constexpr uint32_t TMEM_COLS = CPS == 2 ? 256 : 512;
-  // one query tile per CTA, e4m3: a second S buffer after O (see the header)
+  // one query tile per CTA: a second S buffer after O (see the header)
   static constexpr bool S2 = NT == 1 && CPS == 1 && FA3B_FWD_S2;
+  static_assert(!S2 || 2 * 128 + D <= 512, "S2 TMEM budget");
   // d = 64 tile pair: three S buffers rotate between the two tiles (3 x 128 + 2 x 64
   // columns), so each tile's next S is computed during its softmax (see the header)
   static constexpr bool S3 = NT == 2 && D == 64 && CPS == 1 && FA3B_FWD_S3;
+  static_assert(!S3 || 3 * 128 + 2 * D <= 512, "S3 TMEM budget");
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_KV = NT * TILE_BYTES;
   static constexpr int OFF_BAR = OFF_KV + STAGES * TILE_BYTES;
@@ -586,9 +588,6 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
     // FP8: e4m3 codes of P are P * 448 / 2^thr; exp2(x + log2 pmul) produces them directly
     const float inv_pmul = FP8 ? args.fp8_inv_pmul : 1.f;
     const float lpm = FP8 ? args.fp8_lpm : 0.f;
-#ifndef FA3B_FP8_PREFETCH
-#define FA3B_FP8_PREFETCH 1
-#endif
     // per-block K / V scales of the next block are fetched one iteration ahead
     float ks_next = 1.f, vs_next = 1.f;
     if constexpr (FP8) {
@@ -601,17 +600,12 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       float slj = sl2;
       float vfac = 1.f;  // O rescale for a new V block scale (uniform across the CTA)
       if constexpr (FP8) {
-#if FA3B_FP8_PREFETCH
         slj = sl2 * ks_next;
         const float vs = vs_next;
         if (args.kv_blocked && j + 1 < nt) {
           ks_next = args.k_scale[ks_base + j + 1];
           vs_next = args.v_scale[ks_base + j + 1];
         }
-#else
-        slj = sl2 * args.k_scale[ks_base + (args.kv_blocked ? j : 0)];
-        const float vs = args.v_scale[ks_base + (args.kv_blocked ? j : 0)];
-#endif
         if (vs != v_cur) {
           vfac = v_cur / vs;  // 0 on the first block: O is empty
           v_cur = vs;
