@@ -63,9 +63,11 @@ typedef enum fa3b_dtype {
  * schedules (flash_fwd.cpp:142-191). All give results equal within rounding. */
 typedef enum fa3b_schedule {
   FA3B_SCHED_PINGPONG = 0, /* default: 2 query tiles per CTA, softmax of one tile
-                              overlaps the GEMMs of the other (flash_fwd_2stage) */
-  FA3B_SCHED_BASIC = 1,    /* 1 query tile per CTA, no inter-tile overlap
-                              (flash_fwd_basic) */
+                              overlaps the GEMMs of the other (flash_fwd_2stage);
+                              d = 256 always runs one tile with two S buffers */
+  FA3B_SCHED_BASIC = 1,    /* 1 query tile per CTA; its next QK^T overlaps its own
+                              softmax through a second S buffer in TMEM
+                              (flash_fwd_basic semantics) */
   FA3B_SCHED_3STAGE = 2    /* accepted for flash_fwd_3stage; runs PINGPONG */
 } fa3b_schedule;
 
