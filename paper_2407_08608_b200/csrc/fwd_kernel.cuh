@@ -69,6 +69,9 @@
 #ifndef FA3B_FWD_S2
 #define FA3B_FWD_S2 1
 #endif
+#ifndef FA3B_FWD_PV_PRE
+#define FA3B_FWD_PV_PRE 1
+#endif
 #ifndef FA3B_FWD_S3
 #define FA3B_FWD_S3 1
 #endif
@@ -386,6 +389,29 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
                             (acc || k > 0) ? 1u : 0u);
         }
       };
+      // PV with its operand descriptors computed before the wait for P (pinned by an
+      // empty asm so they are not sunk below it): only the MMA issue follows P
+      auto issue_pv_pre = [&](int t, int slot, bool acc, int scol, uint64_t* p_bar, uint32_t par) {
+        constexpr int KS = 128 / KSTEP;
+        uint64_t bd[KS];
+        uint32_t ta[KS];
+#pragma unroll
+        for (int k = 0; k < KS; ++k) {
+          bd[k] = ptx::sw128_desc(kv_addr + slot * T::TILE_BYTES + k * KSTEP * 128, T::CHUNK_BYTES, 1024);
+          ta[k] = tmem + scol + k * 8;
+          asm volatile("" : "+l"(bd[k]), "+r"(ta[k]));
+        }
+        const uint32_t to = tmem + T::o_col(t);
+        ptx::mbar_wait(p_bar, par);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < KS; ++k) {
+          if constexpr (FP8)
+            ptx::mma_f8_ts(to, ta[k], bd[k], idesc_pv, (acc || k > 0) ? 1u : 0u);
+          else
+            ptx::mma_f16_ts(to, ta[k], bd[k], idesc_pv, (acc || k > 0) ? 1u : 0u);
+        }
+      };
       int kvi = 0;  // ring position of this item's K_0
       int itl = 0;
       int pc[NT];   // p_full phases consumed per tile
@@ -419,10 +445,8 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
           }
           for (int j = 0; j < n; ++j) {
             const int slot_v = wait_pos();
-            ptx::mbar_wait(&p_full[0], pc[0]++ & 1);
+            issue_pv_pre(0, slot_v, j > 0, T::s2_col((g0 + j) & 1), &p_full[0], pc[0]++ & 1);
             if (itl == 0) FA3B_TP(0, j, 6);
-            ptx::tc_fence_after();
-            issue_pv(0, slot_v, j > 0, T::s2_col((g0 + j) & 1));
             ptx::mma_commit(&pv_done[0]);
             ptx::mma_commit(&kv_empty[slot_v]);
             if (j + 1 == n) ptx::mma_commit(&o_full[0]);
@@ -526,10 +550,15 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
 #pragma unroll
           for (int t = 0; t < NT; ++t) {
             if (j >= w.n_t[t]) continue;
+#if FA3B_FWD_PV_PRE
+            issue_pv_pre(t, slot_v, j > 0, T::s_col(t), &p_full[t], pc[t]++ & 1);
+            if (itl == 0) FA3B_TP(t, j, 6);
+#else
             ptx::mbar_wait(&p_full[t], pc[t]++ & 1);
             if (itl == 0) FA3B_TP(t, j, 6);
             ptx::tc_fence_after();
             issue_pv(t, slot_v, j > 0, T::s_col(t));
+#endif
             if (j + 1 < w.n_t[t]) {
               if (!k_ready) {
                 ptx::mbar_wait(&kv_full[slot_k], (item_k / T::STAGES) & 1);
