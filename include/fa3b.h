@@ -60,15 +60,27 @@ typedef enum fa3b_dtype {
 } fa3b_dtype;
 
 /* Kernel schedule, the device analogue of the reference's three forward
- * schedules (flash_fwd.cpp:142-191). All give results equal within rounding. */
+ * schedules (flash_fwd.cpp:142-191) plus the paper's ablation variants
+ * (PAPER.md:748-765). All give results equal within rounding; the default is
+ * the fastest. "Tile" = 128 query rows; "S" = the QK^T block in TMEM. */
 typedef enum fa3b_schedule {
-  FA3B_SCHED_PINGPONG = 0, /* default: 2 query tiles per CTA, softmax of one tile
-                              overlaps the GEMMs of the other (flash_fwd_2stage);
-                              d = 256 always runs one tile with two S buffers */
-  FA3B_SCHED_BASIC = 1,    /* 1 query tile per CTA; its next QK^T overlaps its own
-                              softmax through a second S buffer in TMEM
-                              (flash_fwd_basic semantics) */
-  FA3B_SCHED_3STAGE = 2    /* accepted for flash_fwd_3stage; runs PINGPONG */
+  FA3B_SCHED_PINGPONG = 0, /* default (flash_fwd_2stage): d <= 128 runs 2 query tiles per
+                              CTA whose softmax and GEMMs alternate on the tensor core
+                              (inter-warpgroup ping-pong); d = 256 runs
+                              the 3STAGE schedule (two tiles do not fit TMEM) */
+  FA3B_SCHED_BASIC = 1,    /* flash_fwd_basic: one tile per SM, strictly serial
+                              S_j -> softmax_j -> PV_j (flash_fwd.cpp:142-147); warp
+                              specialized, no GEMM-softmax overlap */
+  FA3B_SCHED_3STAGE = 2,   /* flash_fwd_3stage: one tile, S_{j+1} in flight during softmax_j,
+                              which also overlaps PV_{j-1}; the O rescale is deferred to
+                              just before PV_j (two live P blocks, flash_fwd.cpp:170-191) */
+  FA3B_SCHED_2STAGE = 3,   /* the reference's 2-stage order on one tile: S_{j+1} in flight
+                              during softmax_j, softmax_j starts after PV_{j-1} completes
+                              (one pending score, one live P block, flash_fwd.cpp:148-169) */
+  FA3B_SCHED_NO_WS = 4,    /* ablation: GEMM-softmax pipelining (S_{j+1} during softmax_j)
+                              without warp specialization: the softmax warps issue the TMA
+                              loads and MMAs themselves; f16/bf16 only */
+  FA3B_SCHED_LAST = FA3B_SCHED_NO_WS
 } fa3b_schedule;
 
 typedef enum fa3b_status {
@@ -89,6 +101,8 @@ typedef enum fa3b_status {
   FA3B_ERR_WORKSPACE = -14,        /* workspace missing or too small */
   FA3B_ERR_STRUCT = -15,           /* struct_size does not match this library */
   FA3B_ERR_BLOCK = -16,            /* fp8 quantization block size unsupported */
+  FA3B_ERR_SCHEDULE = -17,         /* schedule value unknown or unsupported for the dtype */
+  FA3B_ERR_SCALES = -18,           /* fp8 scale arrays do not match the block sizes */
   FA3B_ERR_CUDA = -100,            /* CUDA error; see fa3b_last_cuda_error() */
   FA3B_ERR_DEVICE = -101           /* device is not sm_100 */
 } fa3b_status;
@@ -149,7 +163,9 @@ typedef struct fa3b_bwd_params {
   const float* lse;     /* [batch, heads_q, seqlen] from fa3b_fwd */
   double alpha;
   int32_t causal;
-  int32_t deterministic; /* reserved; 0 */
+  int32_t deterministic; /* 0: dQ tiles summed in arrival order (fastest);
+                            1: in ascending KV-tile order, the reference's
+                            (flash_bwd.cpp:58-61): reruns are bitwise identical */
   void* workspace;       /* >= fa3b_bwd_workspace_bytes(...) bytes, 256-byte aligned */
   size_t workspace_bytes;
   void* stream;

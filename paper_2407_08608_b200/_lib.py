@@ -15,9 +15,16 @@ PKG_DIR = Path(__file__).resolve().parent
 LIB_PATH = PKG_DIR / "libfa3b.so"
 
 F16, BF16, E4M3, F32 = 0, 1, 2, 3
-SCHED_PINGPONG, SCHED_BASIC, SCHED_3STAGE = 0, 1, 2
+SCHED_PINGPONG, SCHED_BASIC, SCHED_3STAGE, SCHED_2STAGE, SCHED_NO_WS = 0, 1, 2, 3, 4
 
 OK = 0
+ERR_EMPTY = -1
+ERR_HEAD_DIM_MISMATCH = -2
+ERR_SEQLEN_MISMATCH = -3
+ERR_DTYPE = -8
+ERR_DO_SHAPE = -10
+ERR_FWD_SHAPE = -11
+ERR_SCALES = -18
 ERR_CUDA = -100
 
 

@@ -13,6 +13,7 @@ import hashlib
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
@@ -53,13 +54,22 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> Path:
     if (not force and out.exists() and compat.exists() and stamp.exists()
             and stamp.read_text() == digest):
         return out
-    srcs = [str(CSRC / s) for s in CUDA_SOURCES if (CSRC / s).exists()]
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-           "-Xcompiler", "-fvisibility=hidden", "-shared", "-Xlinker", "--no-undefined", "-I", str(ROOT / "include"),
-           "-o", str(out), *srcs]
+    # one nvcc per translation unit, in parallel, then one link
+    objdir = ROOT / "build" / "obj"
+    objdir.mkdir(parents=True, exist_ok=True)
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+             "-Xcompiler", "-fvisibility=hidden", "-I", str(ROOT / "include")]
     if verbose_ptxas:
-        cmd.insert(1, "-Xptxas=-v")
-    _run(cmd)
+        flags.insert(0, "-Xptxas=-v")
+    jobs = []
+    for name in CUDA_SOURCES:
+        src = CSRC / name
+        if src.exists():
+            jobs.append((src, objdir / (src.stem + ".o")))
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 4))) as ex:
+        list(ex.map(lambda j: _run([NVCC, *flags, "-c", "-o", str(j[1]), str(j[0])]), jobs))
+    _run([NVCC, *ARCH, "-shared", "-Xlinker", "--no-undefined", "-o", str(out),
+          *[str(o) for _, o in jobs], "-lcuda"])
     csrcs = [str(CSRC / s) for s in COMPAT_SOURCES if (CSRC / s).exists()]
     if csrcs:
         _run(["g++", "-O2", "-std=c++20", "-Wall", "-fPIC", "-shared", "-I", str(ROOT / "include"),

@@ -17,8 +17,11 @@
 //   dQ_i = dS K       (tcgen05 SS: dS staged in shared memory, MN-major A)
 // dV and dK stay in TMEM for the whole CTA; dQ_i is drained by the softmax
 // warpgroups with red.global.add.v4.f32 into an fp32 workspace (the dQ-writer
-// role). The reference's deterministic ascending-j dQ order
-// is not kept (atomics); results equal it within rounding.
+// role). By default the KV tiles' dQ contributions land in
+// any order (results equal the reference within rounding); with
+// fa3b_bwd_params.deterministic = 1 every dQ tile takes them in ascending KV
+// order behind a per-tile semaphore, the reference's order (flash_bwd.cpp:58-61),
+// so reruns are bitwise identical.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -119,6 +122,7 @@ struct BwdArgs {
   const float* lse2;   // [B, H, Npad]
   const float* delta;  // [B, H, Npad]
   float* dq_acc;       // [B, H, Npad, D]
+  int* dq_sem;         // deterministic mode: [B, H, Npad / 128] adds done per dQ tile, else null
   void* dk;
   long long dk_sb, dk_ss, dk_sh;
   void* dv;
@@ -193,6 +197,19 @@ struct BwdTraits {
   static constexpr int EMU = D == 64 ? FA3B_BWD_EMU64 : FA3B_BWD_EMU128;
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 };
+
+// Deterministic dQ: wait until `want` KV tiles have added into this dQ tile, then
+// order the coming TMA reduce-adds after that observation; after issuing them,
+// wait for their writes, order them before the release, and count this tile.
+__device__ __forceinline__ void sem_wait(const int* sem, int want) {
+  while (ptx::ld_acquire_gpu(sem) != want) ptx::nanosleep(64);
+  ptx::fence_proxy_async_global();
+}
+__device__ __forceinline__ void sem_release(int* sem) {
+  ptx::bulk_wait_group<0>();
+  ptx::fence_proxy_async_global();
+  ptx::red_release_add_gpu(sem, 1);
+}
 
 // TMEM column of the 16-bit P^T / dS^T pairs for K step t (16 query columns):
 // warpgroup w wrote its 64 columns as 32 packed columns at offset 64 w.
@@ -480,6 +497,12 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
     for (int it = 0; it < w.n_iter; ++it, ++gi) {
       const int h = w.hkv * args.group + it / w.per_head;
       const int i = w.i0 + it % w.per_head;
+      // deterministic mode: dQ tile (b, h, i) takes the KV tiles' contributions in
+      // ascending j, the reference's order (flash_bwd.cpp:58-61): KV tile j adds
+      // once the semaphore shows the j tiles before it have landed
+      int* sem = args.dq_sem == nullptr
+                     ? nullptr
+                     : args.dq_sem + (static_cast<size_t>(b) * args.H + h) * (args.Npad / 128) + i;
       ptx::mbar_wait(dq_full, gi & 1);
       if (itl == 0 && dw == 0 && lane == 0) BWD_TP(it, 12);
       ptx::tc_fence_after();
@@ -506,8 +529,10 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
           ptx::fence_proxy_async_smem();
           ptx::named_bar_sync(3, 128);
           if (leader) {
+            if (c == 0 && sem != nullptr) sem_wait(sem, w.j);
             ptx::tma_reduce_add_4d(&tmDQ, smem + T::OFF_STG + (c & 1) * T::CHUNK_BYTES, 32 * c, h, i * 128, b);
             ptx::bulk_commit_group();
+            if (c == NB - 1 && sem != nullptr) sem_release(sem);
           }
         }
       } else {
@@ -525,10 +550,12 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
         ptx::fence_proxy_async_smem();
         ptx::named_bar_sync(3, 128);
         if (leader) {
+          if (sem != nullptr) sem_wait(sem, w.j);
 #pragma unroll
           for (int c = 0; c < NB; ++c)
             ptx::tma_reduce_add_4d(&tmDQ, smem + T::OFF_STG + c * T::CHUNK_BYTES, 32 * c, h, i * 128, b);
           ptx::bulk_commit_group();
+          if (sem != nullptr) sem_release(sem);
         }
       }
     }
@@ -678,22 +705,29 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
 
 size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
+// dQaccum fp32 [B, H, Npad, D] | dQ semaphores int32 [B, H, Npad / 128] (zeroed with
+// dQaccum by one memset) | LSE2 [B, H, Npad] | D [B, H, Npad]
 struct Workspace {
   float* dq_acc;
+  int* dq_sem;
   float* lse2;
   float* delta;
+  size_t zero_bytes;  // dQaccum + semaphores
   size_t bytes;
 };
 
 Workspace carve(void* base, int B, int H, int Npad, int D) {
   Workspace w{};
   const size_t dq = align256(static_cast<size_t>(B) * H * Npad * D * 4);
+  const size_t sem = align256(static_cast<size_t>(B) * H * (Npad / 128) * 4);
   const size_t vec = align256(static_cast<size_t>(B) * H * Npad * 4);
   uint8_t* p = static_cast<uint8_t*>(base);
   w.dq_acc = reinterpret_cast<float*>(p);
-  w.lse2 = reinterpret_cast<float*>(p + dq);
-  w.delta = reinterpret_cast<float*>(p + dq + vec);
-  w.bytes = dq + 2 * vec;
+  w.dq_sem = reinterpret_cast<int*>(p + dq);
+  w.lse2 = reinterpret_cast<float*>(p + dq + sem);
+  w.delta = reinterpret_cast<float*>(p + dq + sem + vec);
+  w.zero_bytes = dq + sem;
+  w.bytes = dq + sem + 2 * vec;
   return w;
 }
 
@@ -724,6 +758,7 @@ int launch_bwd_main(const fa3b_bwd_params& p, const Workspace& ws, int Npad, cud
   a.lse2 = ws.lse2;
   a.delta = ws.delta;
   a.dq_acc = ws.dq_acc;
+  a.dq_sem = p.deterministic ? ws.dq_sem : nullptr;
   a.dk = p.dk.ptr;
   a.dk_sb = p.dk.stride_batch;
   a.dk_ss = p.dk.stride_seq;
@@ -795,7 +830,9 @@ int fa3b_bwd_preprocess(const fa3b_bwd_preprocess_params* pp) {
   if (!p.o.ptr || !p.dout.ptr || !p.delta) return FA3B_ERR_NULL;
   if (p.dtype != FA3B_DTYPE_BF16 && p.dtype != FA3B_DTYPE_F16 && p.dtype != FA3B_DTYPE_F32)
     return FA3B_ERR_DTYPE;
-  int rc = launch_prep(p.o, p.dout, p.dtype, p.batch, p.heads, p.seqlen, p.head_dim, p.seqlen, p.delta,
+  int rc = check_device();
+  if (rc != FA3B_OK) return rc;
+  rc = launch_prep(p.o, p.dout, p.dtype, p.batch, p.heads, p.seqlen, p.head_dim, p.seqlen, p.delta,
                        nullptr, nullptr, static_cast<cudaStream_t>(p.stream));
   if (rc == FA3B_OK) g_last_launch_count = 1;
   return rc;
@@ -822,8 +859,10 @@ int fa3b_bwd(const fa3b_bwd_params* pp) {
   const Workspace ws = carve(p.workspace, B, H, Npad, D);
   if (p.workspace == nullptr || p.workspace_bytes < ws.bytes || !aligned16(p.workspace))
     return FA3B_ERR_WORKSPACE;
+  if ((rc = check_device()) != FA3B_OK) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(p.stream);
-  cudaError_t e = cudaMemsetAsync(ws.dq_acc, 0, static_cast<size_t>(B) * H * Npad * D * 4, st);
+  if (p.deterministic != 0 && p.deterministic != 1) return FA3B_ERR_DTYPE;
+  cudaError_t e = cudaMemsetAsync(ws.dq_acc, 0, p.deterministic ? ws.zero_bytes : static_cast<size_t>(B) * H * Npad * D * 4, st);
   if (e != cudaSuccess) return cuda_fail(e);
   if ((rc = launch_prep(p.o, p.dout, p.dtype, B, H, N, D, Npad, ws.delta, p.lse, ws.lse2, st)) != FA3B_OK)
     return rc;

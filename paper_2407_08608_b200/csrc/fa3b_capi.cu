@@ -59,20 +59,25 @@ bool fwd_pairing_impl(int head_dim, bool causal, bool fp8) {
   return forced == 1;  // warp pairing measured faster on every C2/C3/C5 shape
 }
 
+}  // namespace
+
+// sm_100 check, cached per device (a process may drive several GPUs) and made by
+// every entry point that launches kernels.
 int check_device() {
-  static int status = [] {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return static_cast<int>(FA3B_ERR_DEVICE);
+  static std::mutex mu;
+  static std::vector<int> cache;  // 0 unknown, 1 ok, 2 unsupported
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return FA3B_ERR_DEVICE;
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev >= static_cast<int>(cache.size())) cache.resize(dev + 1, 0);
+  if (cache[dev] == 0) {
     int major = 0, minor = 0;
     cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
     cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
-    return (major == 10 && minor == 0) ? static_cast<int>(FA3B_OK)
-                                        : static_cast<int>(FA3B_ERR_DEVICE);
-  }();
-  return status;
+    cache[dev] = (major == 10 && minor == 0) ? 1 : 2;
+  }
+  return cache[dev] == 1 ? FA3B_OK : FA3B_ERR_DEVICE;
 }
-
-}  // namespace
 
 bool fwd_pairing(int head_dim, bool causal, bool fp8) { return fwd_pairing_impl(head_dim, causal, fp8); }
 
@@ -265,6 +270,8 @@ const char* fa3b_error_string(int status) {
     case FA3B_ERR_WORKSPACE: return "fa3b: workspace missing or too small";
     case FA3B_ERR_STRUCT: return "fa3b: parameter struct size mismatch (ABI)";
     case FA3B_ERR_BLOCK: return "fa3b: fp8 quantization block must be 0 (per tensor) or 128 rows";
+    case FA3B_ERR_SCHEDULE: return "fa3b: unknown schedule, or schedule unsupported for this dtype";
+    case FA3B_ERR_SCALES: return "fa3b: fp8 scale arrays do not match the quantization blocks";
     case FA3B_ERR_CUDA: return "fa3b: CUDA error (see fa3b_last_cuda_error)";
     case FA3B_ERR_DEVICE: return "fa3b: requires an sm_100 (B200) device";
     default: return "fa3b: unknown status";
@@ -279,6 +286,7 @@ int fa3b_fwd(const fa3b_fwd_params* pp) {
   int rc = validate_problem(p.batch, p.heads_q, p.heads_kv, p.seqlen, p.head_dim, p.alpha);
   if (rc != FA3B_OK) return rc;
   if (!p.q.ptr || !p.k.ptr || !p.v.ptr || !p.o.ptr) return FA3B_ERR_NULL;
+  if (p.schedule < FA3B_SCHED_PINGPONG || p.schedule > FA3B_SCHED_LAST) return FA3B_ERR_SCHEDULE;
   const bool fp8 = p.in_dtype == FA3B_DTYPE_E4M3;
   if (p.in_dtype != FA3B_DTYPE_F16 && p.in_dtype != FA3B_DTYPE_BF16 && !fp8)
     return FA3B_ERR_DTYPE;

@@ -26,6 +26,8 @@ int launch_fwd_fp8(const fa3b_fwd_params& p, cudaStream_t stream);
 int ensure_smem_attr(const void* kernel, int bytes);
 // Streaming multiprocessors of the current device (cached per device).
 int num_sms();
+// FA3B_OK on an sm_100 current device, else FA3B_ERR_DEVICE (cached per device).
+int check_device();
 // Persistent forward grid: one CTA per SM (or per SM slot), never more than the work.
 inline int fwd_grid(int seqlen, int nt, int heads, int batch, int ctas_per_sm) {
   const long long items = static_cast<long long>((seqlen + nt * 128 - 1) / (nt * 128)) * heads * batch;

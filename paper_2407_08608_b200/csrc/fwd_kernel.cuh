@@ -608,7 +608,9 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       const size_t hq = static_cast<size_t>(b) * args.H + h;
       const size_t hk = static_cast<size_t>(b) * args.Hkv + hkv;
       const int nqb_all = (N + 127) / 128;
-      sl2 *= args.q_blocked ? args.q_scale[hq * nqb_all + q_base / 128 + t] : args.q_scale[hq];
+      // a tile past N (nt == 0, odd block count in the pair path) has no scale
+      if (nt > 0)
+        sl2 *= args.q_blocked ? args.q_scale[hq * nqb_all + q_base / 128 + t] : args.q_scale[hq];
       ks_base = static_cast<int>(args.kv_blocked ? hk * nkv : hk);
     }
     float v_cur = 0.f;  // V scale the O accumulator is expressed in (FP8)

@@ -184,6 +184,23 @@ constexpr uint64_t kEvictNormal = 0x1000000000000000ull;
 constexpr uint64_t kEvictLast = 0x14F0000000000000ull;
 
 // ---------------------------------------------------------------- TMEM
+// Ordered global semaphores (the deterministic dQ reduction): an acquire load to
+// spin on, a release increment, and the proxy fence that orders the async-proxy
+// (TMA) reduce-adds with them in both directions.
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add_gpu(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ void nanosleep(uint32_t ns) {
+  asm volatile("nanosleep.u32 %0;" ::"r"(ns));
+}
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -384,20 +401,22 @@ __device__ __forceinline__ float max3(float a, float b, float c) {
   return d;
 }
 // 2^x on the FMA/ALU pipes (frees the MUFU): x = n + f with n = rint(x)
-// (magic-number add), f in [-1/2, 1/2], 2^f by a degree-3 minimax polynomial
-// (max relative error 7.5e-5, below half an ulp of bf16/fp16/e4m3 P), 2^n
-// added into the exponent field. Inputs below -126 flush to ~0 (x = -inf too).
+// (magic-number add), f in [-1/2, 1/2], 2^f by a degree-3 polynomial with
+// p(0) = 1 exactly (minimax otherwise, max relative error 1.0e-4, below half an
+// ulp of bf16/fp16/e4m3 P), 2^n added into the exponent field. Inputs are
+// clamped to -127: there f = 0, p = 1.0 (0x3F800000) and adding -127 << 23 gives
+// exactly +0.0, so masked scores (x = -inf) produce P = 0 as MUFU.EX2 does.
 __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   constexpr float kMagic = 12582912.f;  // 1.5 * 2^23
-  x.x = fmaxf(x.x, -126.f);
-  x.y = fmaxf(x.y, -126.f);
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
   const float2 t = __fadd2_rn(x, make_float2(kMagic, kMagic));
   const float2 r = __fadd2_rn(t, make_float2(-kMagic, -kMagic));
   const float2 f = __ffma2_rn(r, make_float2(-1.f, -1.f), x);
-  float2 p = __ffma2_rn(f, make_float2(0.055171459913253784f, 0.055171459913253784f),
-                        make_float2(0.2426108568906784f, 0.2426108568906784f));
-  p = __ffma2_rn(p, f, make_float2(0.6932609677314758f, 0.6932609677314758f));
-  p = __ffma2_rn(p, f, make_float2(0.9999281167984009f, 0.9999281167984009f));
+  float2 p = __ffma2_rn(f, make_float2(0.05500893294811249f, 0.05500893294811249f),
+                        make_float2(0.24221095442771912f, 0.24221095442771912f));
+  p = __ffma2_rn(p, f, make_float2(0.6932829022407532f, 0.6932829022407532f));
+  p = __ffma2_rn(p, f, make_float2(1.f, 1.f));
   return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
                      __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
 }

@@ -97,6 +97,8 @@ def _fwd_params(**kw):
     ({"in_dtype": 3}, -8, "dtype"),
     ({"q": _lib.Tensor4(4098, 2 * 64 * 128, 2 * 64, 64)}, -7, "16-byte aligned"),
     ({"k": _lib.Tensor4(0, 0, 0, 0)}, -9, "NULL"),
+    ({"schedule": 5}, -17, "unknown schedule"),
+    ({"schedule": -1}, -17, "unknown schedule"),
 ])
 def test_fwd_validation_errors(fa3b_lib, overrides, status, message):
     p = _fwd_params(**overrides)

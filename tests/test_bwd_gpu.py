@@ -127,7 +127,8 @@ def test_bwd_corrupted_lse_is_quiet_but_wrong(port, cuda):
 
 
 def test_bwd_dkdv_deterministic(port, cuda):
-    """dK/dV accumulate in TMEM in a fixed order -> bitwise repeatable."""
+    """dK/dV accumulate in TMEM in a fixed order -> bitwise repeatable even in the
+    default (arrival-order dQ) mode."""
     from paper_2407_08608_b200 import api
     import torch
     q, k, v, do = (to_dev(x, torch.bfloat16)
@@ -137,6 +138,31 @@ def test_bwd_dkdv_deterministic(port, cuda):
     b = api.bwd(q, k, v, o, do, lse, causal=True)
     assert torch.equal(a[1], b[1]) and torch.equal(a[2], b[2])
     assert (a[0].float() - b[0].float()).abs().max().item() < 1e-2
+
+
+@pytest.mark.parametrize("B,H,Hkv,N,D,causal", [
+    (1, 4, 2, 640, 128, True), (2, 8, 8, 2048, 128, False), (1, 16, 4, 3000, 64, True),
+    (2, 16, 16, 8192, 64, False), (1, 32, 32, 4096, 128, True)])
+def test_bwd_deterministic_mode_bitwise(port, cuda, B, H, Hkv, N, D, causal):
+    """deterministic=True: every dQ tile takes its KV tiles' contributions in
+    ascending order (flash_bwd.cpp:58-61), so dQ, dK and dV are bitwise equal
+    across reruns (test_flash_bwd.cpp:121-131) — on shapes with many KV tiles
+    per dQ tile and several persistent rounds — and within the usual tolerance
+    of the arrival-order result."""
+    from paper_2407_08608_b200 import api
+    import torch
+    gen = torch.Generator(device="cuda").manual_seed(N + D + H)
+    q, do = (torch.randn(B, N, H, D, device="cuda", generator=gen).bfloat16() for _ in range(2))
+    k, v = (torch.randn(B, N, Hkv, D, device="cuda", generator=gen).bfloat16() for _ in range(2))
+    o, lse = api.fwd(q, k, v, causal=causal)
+    runs = [api.bwd(q, k, v, o, do, lse, causal=causal, deterministic=True) for _ in range(3)]
+    for r in runs[1:]:
+        for x, y in zip(runs[0], r):
+            assert torch.equal(x, y)
+    fast = api.bwd(q, k, v, o, do, lse, causal=causal)
+    scale = fast[0].float().abs().max().item()
+    assert (runs[0][0].float() - fast[0].float()).abs().max().item() <= 1e-2 * scale
+    assert torch.equal(runs[0][1], fast[1]) and torch.equal(runs[0][2], fast[2])
 
 
 def test_bwd_preprocess_matches_numpy(port, cuda):
