@@ -2,18 +2,25 @@
 TFLOPs/s vs seqlen at hdim 128, % of B200 tensor peak).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload c2|c5] [--dtype bf16|e4m3]
 
-Step = one forward pass of the C2 workload shard (BF16, hdim 128, seqlen
-8192, batch 2 x 16 heads = 16k tokens, hidden 2048, non-causal) through the
-C ABI (fa3b_fwd). Multi-GPU (torchrun) is weak scaling: every rank runs its
-own batch shard, no data-path collective (attention shards by batch x head);
-the only cross-rank traffic is the barrier and the max-over-ranks of the
-device time.
+Step = one forward pass of the workload through the C ABI (fa3b_fwd):
+  c2 (default)  C2 shard: BF16, hdim 128, seqlen 8192, batch 2 x 16 heads = 16k
+                tokens (hidden 2048), non-causal. Multi-GPU: weak scaling, every
+                rank its own batch shard.
+  c5            Llama-3-70B attention (64 query / 8 KV heads, hdim 128, seqlen
+                8192, batch 1, causal). Multi-GPU: strong scaling, each rank the
+                fa3b_fwd of its whole KV-head groups on strided views of the
+                full tensors (shard.shard_forward).
+--dtype e4m3 runs the FP8 forward (K6) on operands prepared by K5 (per-block
+scales, Hadamard on Q/K); its e2e leg includes the three K5 launches.
+Attention shards by batch x head with no exchange step: the only cross-rank
+traffic is the barrier and the max-over-ranks of the device time.
 
 --impl reference times the reference's own CPU implementation
 (oracle/_ref/libflashlab_ref.so = flashlab flash_fwd_2stage compiled from
 its sources; the C restatement if that library is absent) on the same
-workload, one (batch, head) unit per host process.
+workload at the same seqlen, one (batch, head) unit per host process.
 """
 from __future__ import annotations
 
@@ -30,8 +37,13 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "attention fwd/bwd TFLOPs/s (BF16, FP8) vs seqlen at hdim 128; % of B200 tensor peak"
-WORKLOAD = dict(name="C2 bf16 fwd hdim128 seqlen8192", batch=2, heads=16, heads_kv=16,
-                seqlen=8192, head_dim=128, causal=False)
+WORKLOADS = {
+    "c2": dict(name="C2 bf16 fwd hdim128 seqlen8192", batch=2, heads=16, heads_kv=16,
+               seqlen=8192, head_dim=128, causal=False, scaling="weak"),
+    "c5": dict(name="C5 Llama-3-70B GQA 64/8 fwd hdim128 seqlen8192 (KV-head sharded)",
+               batch=1, heads=64, heads_kv=8, seqlen=8192, head_dim=128, causal=True,
+               scaling="strong"),
+}
 
 
 def flops_fwd(B, H, N, D, causal):
@@ -49,11 +61,13 @@ def measured_peaks():
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """NVML sampling of SM clock and throttle reasons during the timed region."""
+    """NVML sampling (every ~1 ms) of the SM clock and throttle reasons while
+    the timed region runs."""
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period: float = 0.001):
         self.samples = []
         self.reasons = set()
+        self.period = period
         self._stop = threading.Event()
         self._t = None
         self.max_mhz = None
@@ -84,7 +98,7 @@ class ClockSampler:
                         self.reasons.add(k)
             except Exception:  # noqa: BLE001
                 pass
-            time.sleep(0.01)
+            time.sleep(self.period)
 
     def __enter__(self):
         if self.nv is not None:
@@ -99,8 +113,8 @@ class ClockSampler:
 
     def summary(self):
         s = sorted(self.samples)
-        return {"sm_mhz": s[len(s) // 2] if s else None, "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(s)}
+        return {"sm_mhz": s[len(s) // 2] if s else None, "sm_min_mhz": s[0] if s else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(s)}
 
 
 # ------------------------------------------------------------ reference arm
@@ -130,7 +144,8 @@ def _ref_worker_run(causal):
 
 class CpuReference:
     """The reference CPU path: one (batch, head) unit per process, P processes
-    (threads in one process scale poorly)."""
+    (threads in one process scale poorly). The parent process
+    loads the same library (so it is visibly the code that ran)."""
 
     def __init__(self, n, d, causal, procs=None):
         import multiprocessing as mp
@@ -138,6 +153,7 @@ class CpuReference:
         import oracle as O
         self.use_ref = O.Ref.available()
         self.kind = "reference" if self.use_ref else "port"
+        self.lib = O.Ref() if self.use_ref else O.Port()  # loaded here too
         self.n, self.d, self.causal = n, d, causal
         self.procs = procs or len(os.sched_getaffinity(0)) or 1
         ctx = mp.get_context("spawn")
@@ -153,9 +169,10 @@ class CpuReference:
         return flops_fwd(1, 1, self.n, self.d, self.causal) * self.procs
 
     def sample_desc(self):
-        lib = "oracle/_ref flashlab flash_fwd_2stage" if self.use_ref else "oracle port"
-        return (f"{self.procs} processes x 1 (batch, head) unit each: N={self.n}, d={self.d}, "
-                f"causal={int(self.causal)}, FP64, tile 64x64 ({lib})")
+        lib = ("oracle/_ref/libflashlab_ref.so flashlab::flash_fwd_2stage" if self.use_ref
+               else "oracle port (C restatement)")
+        return (f"{self.procs} processes x 1 (batch, head) unit each per step: N={self.n}, "
+                f"d={self.d}, causal={int(self.causal)}, FP64, tile 64x64 ({lib})")
 
     def close(self):
         self.pool.terminate()
@@ -174,12 +191,11 @@ def cpu_model():
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
-    w = WORKLOAD
-    # Bound the whole run to a few minutes: a unit at N=8192 costs ~6 s of one
-    # core; shorter sequence samples keep the same per-core FLOP rate.
-    total = args.steps + args.warmup
-    n_s = w["seqlen"] if total <= 20 else (4096 if total <= 80 else 2048)
-    ref = CpuReference(n_s, w["head_dim"], w["causal"])
+    w = WORKLOADS[args.workload]
+    # The reference's per-unit cost does not depend on how many units the workload
+    # has, so a step is a bounded sample: one unit per host core at the workload's
+    # own seqlen (~4.5 s of FP64 per unit at N = 8192, d = 128).
+    ref = CpuReference(w["seqlen"], w["head_dim"], w["causal"])
     try:
         for _ in range(args.warmup):
             ref.step()
@@ -191,11 +207,11 @@ def run_reference(args, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": w["scaling"],
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": w["name"], "global_batch": w["batch"] * world,
-                   "seq_len": w["seqlen"], "heads": w["heads"], "head_dim": w["head_dim"],
-                   "causal": w["causal"], "parallelism": "host processes",
+        "config": {"workload": w["name"], "global_batch": w["batch"], "seq_len": w["seqlen"],
+                   "heads": w["heads"], "heads_kv": w["heads_kv"], "head_dim": w["head_dim"],
+                   "causal": w["causal"], "parallelism": f"{ref.procs} host processes",
                    "cpu": cpu_model()},
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": ref.procs,
                          "kind": ref.kind, "sample": ref.sample_desc()},
@@ -206,32 +222,28 @@ def run_reference(args, rank, world):
     return 0
 
 
-# ------------------------------------------------------------------- our arm
-def time_fwd(api, torch, q, k, v, causal, iters, warmup, stream):
-    for _ in range(warmup):
-        api.fwd(q, k, v, causal=causal, stream=stream)
-    torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(iters)]
-    for a, b in ev:
-        a.record(stream)
-        api.fwd(q, k, v, causal=causal, stream=stream)
-        b.record(stream)
-    torch.cuda.synchronize()
-    return sum(a.elapsed_time(b) for a, b in ev) / iters
-
-
-def _time(fn, torch, stream, iters=10, warmup=3):
+# ------------------------------------------------------------------- timing
+def _timed(fn, torch, stream, min_ms=200.0, warmup=3, max_iters=2000):
+    """Average ms of fn() over a loop of >= min_ms of device time (CUDA events on
+    `stream`), with the clocks sampled during that loop."""
     for _ in range(warmup):
         fn()
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(stream)
-    for _ in range(iters):
-        fn()
+    fn()
     b.record(stream)
     torch.cuda.synchronize()
-    return a.elapsed_time(b) / iters
+    one = max(a.elapsed_time(b), 1e-3)
+    iters = int(min(max_iters, max(5, math.ceil(min_ms / one))))
+    sampler = ClockSampler(torch.cuda.current_device())
+    with sampler:
+        a.record(stream)
+        for _ in range(iters):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+    return a.elapsed_time(b) / iters, iters, sampler.summary()
 
 
 def fp8_peak_tflops(torch, dev):
@@ -256,105 +268,175 @@ def fp8_peak_tflops(torch, dev):
     return 2 * n ** 3 / best / 1e9
 
 
-def sweep(api, torch, dev, stream):
-    """C2 sweep (16k tokens per point, hidden 2048), C3 FP8, C4 backward, C5 (Llama-3-70B GQA).
-    Each line carries its fraction of the matching measured peak (bf16: MEASURED_PEAKS.json
-    burst; e4m3: cuBLASLt measured here; fp8_prepare: the measured HBM copy bandwidth)."""
+def _prep3(api, x, stream, seed=1):
+    """K5 on Q, K (Hadamard, per-block scales) and V (per-block scales)."""
+    return [api.fp8_prepare(t, block_rows=128, hadamard=i < 2, seed=seed, stream=stream)
+            for i, t in enumerate(x)]
+
+
+def sweep(api, torch, dev, stream, fp8_peak):
+    """BASELINE.json's curves, one entry per point with its own clocks:
+    C2 BF16 fwd (seqlen 512-16k at 16k tokens, hdim 64/128/256, causal and not),
+    C3 FP8 fwd (K6 alone and the full K5 x 3 + K6 pipeline; K5 alone),
+    C4 BF16 bwd (hdim 64/128, both dQ modes at 8k), C5 (BF16 and FP8), and the
+    paper's Table 3 schedule ablation (B4 N8448 H16 d128 FP16)."""
     out = []
-    pts = [(n, 128, c) for n in (512, 1024, 2048, 4096, 8192, 16384) for c in (False, True)]
-    pts += [(8192, 64, False), (8192, 64, True), (8192, 256, False), (8192, 256, True)]
-    for n, d, causal in pts:
-        B, H = 16384 // n, 2048 // d
-        q, k, v = (torch.randn(B, n, H, d, device=dev, dtype=torch.bfloat16) for _ in range(3))
-        ms = time_fwd(api, torch, q, k, v, causal, 10, 3, stream)
-        out.append({"pass": "fwd", "dtype": "bf16", "seqlen": n, "head_dim": d, "batch": B,
-                    "heads": H, "causal": causal,
-                    "tflops": flops_fwd(B, H, n, d, causal) / ms / 1e9, "ms": ms})
-        del q, k, v
-    # C3: FP8 forward (K6 on prepared e4m3 operands; K5 timed separately)
+    bf16_peak, hbm, _ = measured_peaks()
+    seqlens = (512, 1024, 2048, 4096, 8192, 16384)
+
+    def add(rec, flops=None, bytes_=None, peak=None, fn=None):
+        try:
+            ms, iters, clk = _timed(fn, torch, stream)
+        except Exception as e:  # noqa: BLE001 (an unsupported variant is reported, not fatal)
+            rec["error"] = str(e)[:200]
+            out.append(rec)
+            return
+        rec.update(ms=ms, iters=iters, clocks=clk)
+        if flops is not None:
+            rec["tflops"] = flops / ms / 1e9
+            rec["frac"] = rec["tflops"] / peak
+        if bytes_ is not None:
+            rec["gbs"] = bytes_ / ms / 1e6
+            rec["frac_of_hbm"] = rec["gbs"] / hbm
+        out.append(rec)
+
+    # C2: BF16 forward
+    for d in (128, 64, 256):
+        for n in seqlens:
+            B, H = 16384 // n, 2048 // d
+            q, k, v = (torch.randn(B, n, H, d, device=dev, dtype=torch.bfloat16) for _ in range(3))
+            o = torch.empty_like(q)
+            lse = torch.empty(B, H, n, device=dev)
+            for causal in (False, True):
+                add({"pass": "fwd", "dtype": "bf16", "seqlen": n, "head_dim": d, "batch": B,
+                     "heads": H, "causal": causal}, flops_fwd(B, H, n, d, causal), peak=bf16_peak,
+                    fn=lambda: api.fwd(q, k, v, causal=causal, out=o, lse=lse, stream=stream))
+            del q, k, v, o, lse
+    # C3: FP8 forward
     for d in (128, 256):
-        for causal in (False, True):
-            B, H, n = 2, 2048 // d, 8192
+        for n in seqlens:
+            B, H = 16384 // n, 2048 // d
             x = [torch.randn(B, n, H, d, device=dev, dtype=torch.bfloat16) for _ in range(3)]
-            pr = [api.fp8_prepare(t, block_rows=128, hadamard=i < 2, seed=1, stream=stream)
-                  for i, t in enumerate(x)]
-            ms = _time(lambda: api.fwd(pr[0][0], pr[1][0], pr[2][0], causal=causal,
-                                       q_scale=pr[0][1], k_scale=pr[1][1], v_scale=pr[2][1],
-                                       stream=stream), torch, stream)
-            out.append({"pass": "fwd", "dtype": "e4m3", "seqlen": n, "head_dim": d, "batch": B,
-                        "heads": H, "causal": causal,
-                        "tflops": flops_fwd(B, H, n, d, causal) / ms / 1e9, "ms": ms})
-            if not causal:
-                ms = _time(lambda: api.fp8_prepare(x[0], block_rows=128, hadamard=True, seed=1,
-                                                   stream=stream), torch, stream)
-                out.append({"pass": "fp8_prepare", "head_dim": d, "elements": x[0].numel(),
-                            "gbs": x[0].numel() * 3 / ms / 1e6, "ms": ms})
-            del x, pr
-    # C4: backward (K2-K4 through fa3b_bwd)
+            pr = _prep3(api, x, stream)
+            o = torch.empty(B, n, H, d, device=dev, dtype=torch.bfloat16)
+            lse = torch.empty(B, H, n, device=dev)
+            for causal in (False, True):
+                f = flops_fwd(B, H, n, d, causal)
+                k6 = lambda: api.fwd(pr[0][0], pr[1][0], pr[2][0], causal=causal, out=o, lse=lse,  # noqa: E731
+                                     q_scale=pr[0][1], k_scale=pr[1][1], v_scale=pr[2][1],
+                                     stream=stream)
+                add({"pass": "fwd", "dtype": "e4m3", "kernel": "K6", "seqlen": n, "head_dim": d,
+                     "batch": B, "heads": H, "causal": causal}, f, peak=fp8_peak, fn=k6)
+                if n == 8192:
+                    def pipe():
+                        p = _prep3(api, x, stream)
+                        api.fwd(p[0][0], p[1][0], p[2][0], causal=causal, out=o, lse=lse,
+                                q_scale=p[0][1], k_scale=p[1][1], v_scale=p[2][1], stream=stream)
+                    add({"pass": "fwd", "dtype": "e4m3", "kernel": "K5x3+K6 (full FP8 forward)",
+                         "seqlen": n, "head_dim": d, "batch": B, "heads": H, "causal": causal},
+                        f, peak=fp8_peak, fn=pipe)
+            del x, pr, o, lse
+    for d in (64, 128, 256):  # K5 alone: 2 B in + 1 B out per element
+        x = torch.randn(2, 8192, 2048 // d, d, device=dev, dtype=torch.bfloat16)
+        add({"pass": "fp8_prepare", "head_dim": d, "block_rows": 128, "elements": x.numel()},
+            bytes_=3 * x.numel(),
+            fn=lambda: api.fp8_prepare(x, block_rows=128, hadamard=True, seed=1, stream=stream))
+        del x
+    # C4: backward
     for d in (128, 64):
-        for causal in (False, True):
-            B, H, n = 2, 2048 // d, 8192
+        for n in seqlens:
+            B, H = 16384 // n, 2048 // d
             q, k, v, do = (torch.randn(B, n, H, d, device=dev, dtype=torch.bfloat16)
                            for _ in range(4))
-            o, lse = api.fwd(q, k, v, causal=causal, stream=stream)
-            ws = torch.empty(api.bwd_workspace_bytes(B, H, H, n, d), dtype=torch.uint8,
-                             device=dev)
-            grads = [torch.empty_like(x) for x in (q, k, v)]
-            ms = _time(lambda: api.bwd(q, k, v, o, do, lse, causal=causal, dq=grads[0],
-                                       dk=grads[1], dv=grads[2], workspace=ws, stream=stream),
-                       torch, stream)
-            out.append({"pass": "bwd", "dtype": "bf16", "seqlen": n, "head_dim": d, "batch": B,
-                        "heads": H, "causal": causal,
-                        "tflops": 2.5 * flops_fwd(B, H, n, d, causal) / ms / 1e9, "ms": ms})
-            del q, k, v, do, o, lse, ws, grads
+            ws = torch.empty(api.bwd_workspace_bytes(B, H, H, n, d), dtype=torch.uint8, device=dev)
+            grads = [torch.empty_like(q) for _ in range(3)]
+            for causal in (False, True):
+                o, lse = api.fwd(q, k, v, causal=causal, stream=stream)
+                for det in ((False, True) if n == 8192 else (False,)):
+                    add({"pass": "bwd", "dtype": "bf16", "seqlen": n, "head_dim": d, "batch": B,
+                         "heads": H, "causal": causal, "deterministic": det},
+                        2.5 * flops_fwd(B, H, n, d, causal), peak=bf16_peak,
+                        fn=lambda: api.bwd(q, k, v, o, do, lse, causal=causal, dq=grads[0],
+                                           dk=grads[1], dv=grads[2], workspace=ws,
+                                           deterministic=det, stream=stream))
+            del q, k, v, do, ws, grads, o, lse
+    # C5: Llama-3-70B GQA 64/8
     q = torch.randn(1, 8192, 64, 128, device=dev, dtype=torch.bfloat16)
     k, v = (torch.randn(1, 8192, 8, 128, device=dev, dtype=torch.bfloat16) for _ in range(2))
+    pr = _prep3(api, [q, k, v], stream)
     for causal in (False, True):
-        ms = time_fwd(api, torch, q, k, v, causal, 10, 3, stream)
-        out.append({"pass": "fwd", "dtype": "bf16", "workload": "C5 llama3-70b gqa 64/8",
-                    "seqlen": 8192, "head_dim": 128, "batch": 1, "heads": 64, "heads_kv": 8,
-                    "causal": causal, "tflops": flops_fwd(1, 64, 8192, 128, causal) / ms / 1e9,
-                    "ms": ms})
-    bf16_peak, hbm, _ = measured_peaks()
-    try:
-        fp8_peak = fp8_peak_tflops(torch, dev)
-    except Exception:  # noqa: BLE001
-        fp8_peak = 4500.0
-    for r in out:
-        if r["pass"] == "fp8_prepare":
-            r["frac_of_hbm"] = r["gbs"] / hbm
-        else:
-            r["frac"] = r["tflops"] / (fp8_peak if r["dtype"] == "e4m3" else bf16_peak)
+        f = flops_fwd(1, 64, 8192, 128, causal)
+        add({"pass": "fwd", "dtype": "bf16", "workload": "C5 llama3-70b gqa 64/8", "seqlen": 8192,
+             "head_dim": 128, "batch": 1, "heads": 64, "heads_kv": 8, "causal": causal}, f,
+            peak=bf16_peak, fn=lambda: api.fwd(q, k, v, causal=causal, stream=stream))
+        add({"pass": "fwd", "dtype": "e4m3", "kernel": "K6", "workload": "C5 llama3-70b gqa 64/8",
+             "seqlen": 8192, "head_dim": 128, "batch": 1, "heads": 64, "heads_kv": 8,
+             "causal": causal}, f, peak=fp8_peak,
+            fn=lambda: api.fwd(pr[0][0], pr[1][0], pr[2][0], causal=causal, q_scale=pr[0][1],
+                               k_scale=pr[1][1], v_scale=pr[2][1], stream=stream))
+    del q, k, v, pr
+    # Table 3 analogue: schedule ablation at the paper's shape (FP16, non-causal)
+    B, n, H, d = 4, 8448, 16, 128
+    q, k, v = (torch.randn(B, n, H, d, device=dev, dtype=torch.float16) for _ in range(3))
+    for sched in ("pingpong", "basic", "no_ws", "2stage", "3stage"):
+        add({"pass": "fwd", "dtype": "f16", "workload": "ablation B4 N8448 H16 d128",
+             "schedule": sched, "seqlen": n, "head_dim": d, "batch": B, "heads": H,
+             "causal": False}, flops_fwd(B, H, n, d, False), peak=bf16_peak,
+            fn=lambda: api.fwd(q, k, v, schedule=sched, stream=stream))
+    del q, k, v
     out.append({"peaks": {"bf16_tflops": bf16_peak, "fp8_tflops_measured_cublas": fp8_peak,
                           "hbm_gbs": hbm}})
     return out
 
 
+# ------------------------------------------------------------------- our arm
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
     from paper_2407_08608_b200 import _lib, api
 
-    from paper_2407_08608_b200.shard import max_over_ranks, partition
+    from paper_2407_08608_b200.shard import max_over_ranks, partition, shard_forward
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     lib = _lib.load()
-    w = WORKLOAD
+    w = WORKLOADS[args.workload]
+    fp8 = args.dtype == "e4m3"
     H, Hkv, N, D, causal = (w["heads"], w["heads_kv"], w["seqlen"], w["head_dim"], w["causal"])
-    # weak scaling: the global batch grows with the world; each rank owns whole
-    # (batch, kv-head) units of it and never exchanges data with the others
-    shard = partition(w["batch"] * world, Hkv, world)[rank]
-    b0, b1 = shard.batch_range(Hkv)
-    B = b1 - b0
-    gen = torch.Generator(device=dev).manual_seed(1234 + b0)
+    g = H // Hkv
+    weak = w["scaling"] == "weak"
+    B_all = w["batch"] * (world if weak else 1)
+    shards = partition(B_all, Hkv, world)
+    shard = shards[rank]
+    calls = shard.calls(Hkv)
+    # this rank allocates the batches its shard touches, all heads: its calls run on
+    # strided views (a KV-head slice of C5, or whole batches of C2)
+    b_lo, b_hi = min(c[0] for c in calls), max(c[1] for c in calls)
+    B = b_hi - b_lo
+    local = [type(shard)(shard.rank, tuple((b - b_lo, kv) for b, kv in shard.units))]
+    gen = torch.Generator(device=dev).manual_seed(1234 + b_lo)
     q = torch.randn(B, N, H, D, device=dev, dtype=torch.bfloat16, generator=gen)
     k = torch.randn(B, N, Hkv, D, device=dev, dtype=torch.bfloat16, generator=gen)
     v = torch.randn(B, N, Hkv, D, device=dev, dtype=torch.bfloat16, generator=gen)
     o = torch.empty_like(q)
     lse = torch.empty(B, H, N, device=dev, dtype=torch.float32)
     stream = torch.cuda.Stream(device=dev)
-    step_flops = flops_fwd(B, H, N, D, causal)
+    with torch.cuda.stream(stream):
+        pr = _prep3(api, [q, k, v], stream) if fp8 else None
+    torch.cuda.synchronize()
+    # algorithmic FLOPs: this rank's units, and the whole job's
+    rank_flops = sum(flops_fwd(b1 - b0, (kv1 - kv0) * g, N, D, causal)
+                     for b0, b1, kv0, kv1 in calls)
+    job_flops = sum(flops_fwd(b1 - b0, (kv1 - kv0) * g, N, D, causal)
+                    for s in shards for b0, b1, kv0, kv1 in s.calls(Hkv))
+
+    def step():
+        if fp8:
+            return shard_forward(api.fwd, pr[0][0], pr[1][0], pr[2][0], o, lse, local[0], Hkv,
+                                 causal=causal, q_scale=pr[0][1], k_scale=pr[1][1],
+                                 v_scale=pr[2][1], stream=stream)
+        return shard_forward(api.fwd, q, k, v, o, lse, local[0], Hkv, causal=causal,
+                             stream=stream)
 
     def barrier():
         if world > 1:
@@ -362,7 +444,7 @@ def run_ours(args, rank, world, local_rank):
 
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
-            api.fwd(q, k, v, causal=causal, out=o, lse=lse, stream=stream)
+            step()
     torch.cuda.synchronize()
 
     # ---------------- timed region: exactly K steps, device time, max over ranks
@@ -377,8 +459,8 @@ def run_ours(args, rank, world, local_rank):
         t_all0.record(stream)
         for a, b in ev:
             a.record(stream)
-            api.fwd(q, k, v, causal=causal, out=o, lse=lse, stream=stream)
-            launches += lib.fa3b_last_launch_count()
+            step()
+            launches += len(calls) * lib.fa3b_last_launch_count()
             b.record(stream)
         t_all1.record(stream)
         torch.cuda.synchronize()
@@ -386,16 +468,25 @@ def run_ours(args, rank, world, local_rank):
     total_ms = max_over_ranks(t_all0.elapsed_time(t_all1), device=dev)
     kernel_ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
     ms_per_step = total_ms / args.steps
-    value = step_flops * world / (ms_per_step * 1e-3) / 1e12
+    value = job_flops / (ms_per_step * 1e-3) / 1e12
 
     # ---------------- end to end through the public API with host buffers
-    # Every step copies its own Q/K/V from pinned host memory and reads its O and
-    # LSE back; steps are software-pipelined over three streams (H2D of step i,
-    # the kernel of step i-1 and the D2H of step i-2 overlap; two device slots).
-    qh, kh, vh = (x.cpu().pin_memory() for x in (q, k, v))
-    oh = [torch.empty(o.shape, dtype=o.dtype).pin_memory() for _ in range(2)]
-    lh = [torch.empty(lse.shape, dtype=lse.dtype).pin_memory() for _ in range(2)]
-    slots = [[torch.empty_like(x) for x in (q, k, v, o, lse)] for _ in range(2)]
+    # Every step copies this rank's Q/K/V slice from pinned host memory, runs the
+    # forward (FP8: three K5 launches + K6) and reads its O and LSE back; steps are
+    # software-pipelined over three streams (H2D of step i, the kernels of step
+    # i-1 and the D2H of step i-2 overlap; two device slots).
+    def sl(x, per_q, b0, b1, kv0, kv1):
+        lo, hi = (kv0 * g, kv1 * g) if per_q else (kv0, kv1)
+        return x[b0:b1, :, lo:hi]
+
+    (b0, b1, kv0, kv1) = local[0].calls(Hkv)[0] if len(calls) == 1 else (0, B, 0, Hkv)
+    qh, kh, vh = (sl(x, i == 0, b0, b1, kv0, kv1).cpu().pin_memory() for i, x in enumerate((q, k, v)))
+    Bs, Hs = qh.shape[0], qh.shape[2]
+    oh = [torch.empty(qh.shape, dtype=torch.bfloat16).pin_memory() for _ in range(2)]
+    lh = [torch.empty((Bs, Hs, N), dtype=torch.float32).pin_memory() for _ in range(2)]
+    slots = [[torch.empty_like(x, device=dev) for x in (qh, kh, vh)] +
+             [torch.empty(oh[0].shape, dtype=torch.bfloat16, device=dev),
+              torch.empty(lh[0].shape, dtype=torch.float32, device=dev)] for _ in range(2)]
     s_in, s_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
     ev_in = [torch.cuda.Event() for _ in range(2)]
     ev_done = [torch.cuda.Event() for _ in range(2)]
@@ -403,24 +494,29 @@ def run_ours(args, rank, world, local_rank):
     e2e_steps = max(4, min(args.steps, 12))
 
     def e2e_step(i):
-        sl = i % 2
-        qd, kd, vd, od, ld = slots[sl]
+        sl_ = i % 2
+        qd, kd, vd, od, ld = slots[sl_]
         if i >= 2:
-            s_in.wait_event(ev_done[sl])   # the kernel of step i-2 has read this slot
-            stream.wait_event(ev_out[sl])  # the D2H of step i-2 has read this slot
+            s_in.wait_event(ev_done[sl_])   # the kernels of step i-2 have read this slot
+            stream.wait_event(ev_out[sl_])  # the D2H of step i-2 has read this slot
         with torch.cuda.stream(s_in):
             qd.copy_(qh, non_blocking=True)
             kd.copy_(kh, non_blocking=True)
             vd.copy_(vh, non_blocking=True)
-            ev_in[sl].record(s_in)
-        stream.wait_event(ev_in[sl])
-        api.fwd(qd, kd, vd, causal=causal, out=od, lse=ld, stream=stream)
-        ev_done[sl].record(stream)
-        s_out.wait_event(ev_done[sl])
+            ev_in[sl_].record(s_in)
+        stream.wait_event(ev_in[sl_])
+        if fp8:
+            p = _prep3(api, [qd, kd, vd], stream)
+            api.fwd(p[0][0], p[1][0], p[2][0], causal=causal, out=od, lse=ld, q_scale=p[0][1],
+                    k_scale=p[1][1], v_scale=p[2][1], stream=stream)
+        else:
+            api.fwd(qd, kd, vd, causal=causal, out=od, lse=ld, stream=stream)
+        ev_done[sl_].record(stream)
+        s_out.wait_event(ev_done[sl_])
         with torch.cuda.stream(s_out):
-            oh[sl].copy_(od, non_blocking=True)
-            lh[sl].copy_(ld, non_blocking=True)
-            ev_out[sl].record(s_out)
+            oh[sl_].copy_(od, non_blocking=True)
+            lh[sl_].copy_(ld, non_blocking=True)
+            ev_out[sl_].record(s_out)
 
     for i in range(2):
         e2e_step(i)
@@ -436,40 +532,54 @@ def run_ours(args, rank, world, local_rank):
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / e2e_steps, device=dev)
     h2d = sum(x.numel() * x.element_size() for x in (qh, kh, vh))
     d2h = oh[0].numel() * oh[0].element_size() + lh[0].numel() * lh[0].element_size()
-    torch.testing.assert_close(oh[(e2e_steps - 1) % 2], o.cpu(), rtol=0, atol=0)
+    # the host copy of the last step equals the device-resident result for the same slice
+    torch.testing.assert_close(oh[(e2e_steps - 1) % 2], sl(o, True, b0, b1, kv0, kv1).cpu(),
+                               rtol=0, atol=0)
 
     if rank != 0:
         return 0
     peak, hbm, peak_src = measured_peaks()
-    achieved = step_flops / (kernel_ms * 1e-3) / 1e12
+    if fp8:
+        try:
+            peak, peak_src = fp8_peak_tflops(torch, dev), "cuBLASLt e4m3 8192^3 measured here"
+        except Exception:  # noqa: BLE001
+            peak, peak_src = 4500.0, "nominal dense e4m3 (fallback)"
+    else:
+        peak_src = f"{peak_src} bf16 burst (MEASURED_PEAKS.json)"
+    achieved = rank_flops / (kernel_ms * 1e-3) / 1e12
     traffic = None
     prof = ROOT / "profiles" / "ncu_summary.json"
+    key = {("c2", False): "fwd_c2_d128", ("c2", True): "fwd_fp8_d128",
+           ("c5", False): "fwd_c5", ("c5", True): "fwd_fp8_c5"}[(args.workload, fp8)]
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get("fwd_c2_d128", {}).get("dram_bytes")
+            traffic = json.loads(prof.read_text()).get(key, {}).get("dram_bytes")
         except (ValueError, OSError):
             traffic = None
+    kname = (f"fa3b_fwd_kernel<128,2,{str(causal).lower()},{'e4m3' if fp8 else 'bf16'}>")
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic (torch.randn bf16 Q/K/V on device)",
-        "config": {"workload": w["name"], "global_batch": w["batch"] * world, "seq_len": N,
-                   "heads": H,
-                   "heads_kv": Hkv, "head_dim": D, "causal": causal,
-                   "parallelism": f"batch-sharded x{world} (no collectives)",
+        "higher_is_better": True, "scaling": w["scaling"], "vs_baseline": None,
+        "dtype": "e4m3" if fp8 else "bf16",
+        "data": "synthetic (torch.randn bf16 Q/K/V on device"
+                + ("; e4m3 codes + per-block scales from K5)" if fp8 else ")"),
+        "config": {"workload": w["name"], "global_batch": B_all, "seq_len": N,
+                   "heads": H, "heads_kv": Hkv, "head_dim": D, "causal": causal,
+                   "parallelism": (f"batch-sharded x{world} (no collectives)" if weak else
+                                   f"KV-head-sharded x{world}, strided views (no collectives)"),
+                   "calls_per_rank": len(calls),
                    "l2": "no flush; inputs larger than L2 (Q+K+V+O = "
-                         f"{4 * q.numel() * 2 >> 20} MiB > 126 MB)"},
+                         f"{(2 * q.numel() + 2 * k.numel()) * 2 >> 20} MiB per rank > 126 MB)"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": traffic,
-                     "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json)",
-                     "kernel": "fa3b_fwd_kernel<128,2,false,bf16>",
-                     "algorithmic_flops_per_launch": step_flops,
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "kernel": kname, "algorithmic_flops_per_launch": rank_flops // len(calls),
                      "kernel_ms": kernel_ms},
-        "e2e": {"value": step_flops * world / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+        "e2e": {"value": job_flops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
-                "path": "pinned host bf16 -> H2D -> fa3b_fwd (C ABI) -> D2H O + LSE, "
-                        "3-stream software pipeline (copy engines overlap the kernel)"},
+                "path": "pinned host bf16 -> H2D -> " + ("fa3b_fp8_prepare x3 + " if fp8 else "")
+                        + "fa3b_fwd (C ABI) -> D2H O + LSE, 3-stream software pipeline "
+                          "(copy engines overlap the kernels)"},
         "gpu_launches": launches,
         "clocks": sampler.summary(),
     }
@@ -482,9 +592,13 @@ def run_ours(args, rank, world, local_rank):
         line["cpu_baseline"] = {"value": ref.flops_per_step() / secs / 1e12, "unit": "TFLOP/s",
                                 "cores": ref.procs, "kind": ref.kind,
                                 "sample": ref.sample_desc() + f"; {cpu_model()}"}
-    if world == 1 and not args.no_sweep:
+    if world == 1 and not args.no_sweep and args.workload == "c2" and not fp8:
+        try:
+            fp8_peak = fp8_peak_tflops(torch, dev)
+        except Exception:  # noqa: BLE001
+            fp8_peak = 4500.0
         with torch.cuda.stream(stream):
-            line["sweep"] = sweep(api, torch, dev, stream)
+            line["sweep"] = sweep(api, torch, dev, stream, fp8_peak)
     print(json.dumps(line), flush=True)
     return 0
 
@@ -495,6 +609,8 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", choices=tuple(WORKLOADS), default="c2")
+    ap.add_argument("--dtype", choices=("bf16", "e4m3"), default="bf16")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-procs", type=int, default=None)

@@ -14,6 +14,11 @@
 //   bwd_preprocess / flash_bwd                             flash_bwd.hpp:15-21
 //   QuantGranularity / Fp8AttentionConfig                  fp8_attention.hpp:27-38
 //   preprocess_incoherent / fp8_flash_fwd                  fp8_attention.hpp:41-46
+//   SoftmaxState / SoftmaxStep / online_softmax_step       flash_fwd.hpp:26-41
+//   accumulator_permutation / permute_accumulator /
+//     vtile_transpose                                      fp8_attention.hpp:50-57
+// A link-level drop-in built against the reference's own headers (no namespace
+// switch at all) is paper_2407_08608_b200/dropin/ (INTEGRATION.md).
 //
 // Semantics that differ, by design:
 //   - FP64 inputs are rounded to the device format (bf16 by default, see
@@ -82,6 +87,19 @@ struct TileConfig {
   std::size_t block_rows = 64;
   std::size_t block_cols = 64;
 };
+// flash_fwd.hpp:26-41: the online-softmax state and one block step, the
+// reference's host building block (the device kernels fuse it).
+struct SoftmaxState {
+  std::vector<double> row_max;
+  std::vector<double> row_sum;
+  explicit SoftmaxState(std::size_t rows);
+};
+struct SoftmaxStep {
+  Matrix p_tilde;
+  std::vector<double> rescale;
+};
+SoftmaxStep online_softmax_step(SoftmaxState& state, const Matrix& s_block);
+
 struct FlashFwdStats {
   std::size_t blocks_visited = 0;
   std::size_t blocks_skipped = 0;
@@ -125,6 +143,11 @@ struct Fp8AttentionConfig {
 std::pair<Matrix, Matrix> preprocess_incoherent(const Matrix& q, const Matrix& k,
                                                 std::uint64_t seed);
 ForwardOutput fp8_flash_fwd(const AttentionInputs& in, const Fp8AttentionConfig& cfg);
+// fp8_attention.hpp:50-57: the Hopper accumulator layout helpers (host only;
+// sm_100a consumes V MN-major, so the device needs neither).
+std::vector<std::size_t> accumulator_permutation(std::size_t width);
+Matrix permute_accumulator(const Matrix& block);
+Matrix vtile_transpose(const Matrix& vblock, bool permute_rows = false);
 
 // Device format the FP64 inputs are rounded to (f16 or bf16; default bf16).
 enum class DeviceFormat { f16, bf16 };

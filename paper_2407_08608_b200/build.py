@@ -3,6 +3,10 @@
   libfa3b.so           CUDA kernels + C ABI (include/fa3b.h), sm_100a only
   libfa3b_flashlab.so  C++ host mirror of the reference's flashlab API
                        (include/fa3b/flashlab_compat.hpp) over the C ABI
+  dropin/              link-level drop-in of flashlab::core built against the
+                       reference's own headers, plus the reference's unmodified
+                       acceptance_main.cpp linked to it (only where
+                       /root/reference exists; the outputs travel)
 
 Both are compiled with nvcc/g++ directly (no JIT cache), so the .so files
 travel with the repository snapshot to the GPU box.
@@ -23,7 +27,9 @@ CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.environ.get("NVCC", f"{CUDA_HOME}/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CUDA_SOURCES = ["fa3b_capi.cu", "fwd_fp8.cu", "fp8_prepare.cu", "bwd.cu"]
+CUDA_SOURCES = ["fa3b_capi.cu", "fwd16_d64.cu", "fwd16_d128.cu", "fwd16_d256.cu",
+                "fwd16_sched_bf16_c0.cu", "fwd16_sched_bf16_c1.cu", "fwd16_sched_f16_c0.cu",
+                "fwd16_sched_f16_c1.cu", "fwd_fp8.cu", "fp8_prepare.cu", "bwd.cu"]
 COMPAT_SOURCES = ["flashlab_compat.cpp"]
 
 
@@ -37,6 +43,7 @@ def _digest(paths) -> str:
 
 def _inputs():
     files = list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.cpp"))
+    files += list(CSRC.glob("*.inc"))
     files += list((ROOT / "include").rglob("*.h*"))
     return files
 
@@ -77,7 +84,19 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> Path:
               f"-L{CUDA_HOME}/lib64", "-lcudart", "-Wl,--no-undefined",
               f"-Wl,-rpath,$ORIGIN:{CUDA_HOME}/lib64"])
     stamp.write_text(digest)
+    build_dropin()
     return out
+
+
+def build_dropin() -> Path | None:
+    """The link-level drop-in of flashlab::core (dropin/Makefile): needs the
+    reference tree, so it is built here and its outputs travel with the
+    snapshot; on a box without /root/reference the prebuilt files are used."""
+    root = Path(os.environ.get("FLASHLAB_ROOT", "/root/reference/proj"))
+    if not (root / "core" / "include" / "flashlab" / "flash_fwd.hpp").exists():
+        return None
+    _run(["make", "-s", "-C", str(PKG / "dropin"), f"FLASHLAB_ROOT={root}", "-j8"])
+    return PKG / "dropin" / "libflashlab_core_fa3b.so"
 
 
 if __name__ == "__main__":

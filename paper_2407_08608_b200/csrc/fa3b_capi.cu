@@ -14,7 +14,6 @@
 
 #include "../../include/fa3b.h"
 #include "fa3b_internal.cuh"
-#include "fwd_kernel.cuh"
 
 namespace fa3b {
 
@@ -159,66 +158,6 @@ int validate_problem(int batch, int heads_q, int heads_kv, int seqlen, int head_
   return FA3B_OK;
 }
 
-namespace {
-
-#ifndef FA3B_FWD_EMU_S2_16
-#define FA3B_FWD_EMU_S2_16 2
-#endif
-
-template <int D, int NT, bool CAUSAL, bool BF16, int CPS>
-int launch_fwd16(const fa3b_fwd_params& p, cudaStream_t stream) {
-  using T = FwdTraits<D, NT, 2, CPS>;
-  // one-tile CTAs (S2) own the SM's MUFU: FA3B_FWD_EMU_S2_16 of every 8 exp2 pairs on FMA
-  constexpr int EMU = T::S2 ? FA3B_FWD_EMU_S2_16 : FA3B_FWD_EMU;
-  auto kern = fa3b_fwd_kernel<D, NT, CAUSAL, BF16 ? KIND_BF16 : KIND_F16, CPS, EMU>;
-  int rc = ensure_smem_attr(reinterpret_cast<const void*>(kern), T::SMEM_BYTES);
-  if (rc != FA3B_OK) return rc;
-
-  CUtensorMap tq, tk, tv;
-  if ((rc = make_tmap_4d(&tq, p.q, 2, D, p.heads_q, p.seqlen, p.batch, 64, 128)) != FA3B_OK)
-    return rc;
-  if ((rc = make_tmap_4d(&tk, p.k, 2, D, p.heads_kv, p.seqlen, p.batch, 64, 128)) != FA3B_OK)
-    return rc;
-  if ((rc = make_tmap_4d(&tv, p.v, 2, D, p.heads_kv, p.seqlen, p.batch, 64, 128)) != FA3B_OK)
-    return rc;
-
-  FwdArgs a;
-  a.B = p.batch;
-  a.H = p.heads_q;
-  a.Hkv = p.heads_kv;
-  a.N = p.seqlen;
-  a.group = p.heads_q / p.heads_kv;
-  a.scale_log2 = static_cast<float>(std::fabs(p.alpha) * 1.4426950408889634);
-  a.o = p.o.ptr;
-  a.o_sb = p.o.stride_batch;
-  a.o_ss = p.o.stride_seq;
-  a.o_sh = p.o.stride_head;
-  a.out_f32 = p.out_dtype == FA3B_DTYPE_F32;
-  a.lse = p.lse;
-  a.q_scale = a.k_scale = a.v_scale = nullptr;
-  a.q_blocked = a.kv_blocked = 0;
-  a.fp8_thr = 8.f;
-  const uint32_t fmt = BF16 ? 1u : 0u;
-  const uint32_t idesc_qk = ptx::make_idesc(128, 128, fmt, fmt, false, false, p.alpha < 0);
-  const uint32_t idesc_pv = ptx::make_idesc(128, D, fmt, fmt, false, true, false);
-
-  const int grid = fwd_grid(p.seqlen, NT, p.heads_q, p.batch, CPS);  // persistent CTAs
-  kern<<<grid, T::NUM_THREADS, T::SMEM_BYTES, stream>>>(tq, tk, tv, a, idesc_qk, idesc_pv);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e);
-  g_last_launch_count = 1;
-  return FA3B_OK;
-}
-
-template <int D, int NT, int CPS = 1>
-int launch_fwd16_dt(const fa3b_fwd_params& p, cudaStream_t s) {
-  const bool bf16 = p.in_dtype == FA3B_DTYPE_BF16;
-  if (p.causal)
-    return bf16 ? launch_fwd16<D, NT, true, true, CPS>(p, s) : launch_fwd16<D, NT, true, false, CPS>(p, s);
-  return bf16 ? launch_fwd16<D, NT, false, true, CPS>(p, s) : launch_fwd16<D, NT, false, false, CPS>(p, s);
-}
-
-}  // namespace
 }  // namespace fa3b
 
 using namespace fa3b;
@@ -303,19 +242,23 @@ int fa3b_fwd(const fa3b_fwd_params* pp) {
   if ((rc = check_device()) != FA3B_OK) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(p.stream);
   if (fp8) return launch_fwd_fp8(p, s);
-  const bool basic = p.schedule == FA3B_SCHED_BASIC;
+  if (p.schedule != FA3B_SCHED_PINGPONG) {
+    // the one-tile schedule variants (the reference's basic / 2-stage / 3-stage and
+    // the no-warp-specialization ablation); at d = 256 the default is already 3-stage
+    if (p.head_dim == 256 && p.schedule == FA3B_SCHED_3STAGE)
+      return launch_fwd16_default_d256(p, s, false);
+    const bool bf16 = p.in_dtype == FA3B_DTYPE_BF16;
+    if (p.causal) return bf16 ? launch_fwd16_sched_bf16_c1(p, s) : launch_fwd16_sched_f16_c1(p, s);
+    return bf16 ? launch_fwd16_sched_bf16_c0(p, s) : launch_fwd16_sched_f16_c0(p, s);
+  }
   // Ping-pong pairs: two query tiles of one CTA (warp pairing, the default) or
   // one tile in each of two CTAs per SM (CTA pairing, FA3B_FWD_PAIRING=cta);
   // A/B in profiles/r01m_pairing_ab.log.
   const bool cta_pairs = fwd_pairing(p.head_dim, p.causal != 0, false);
   switch (p.head_dim) {
-    case 64:
-      return basic ? launch_fwd16_dt<64, 1>(p, s)
-                   : (cta_pairs ? launch_fwd16_dt<64, 1, 2>(p, s) : launch_fwd16_dt<64, 2>(p, s));
-    case 128:
-      return basic ? launch_fwd16_dt<128, 1>(p, s)
-                   : (cta_pairs ? launch_fwd16_dt<128, 1, 2>(p, s) : launch_fwd16_dt<128, 2>(p, s));
-    case 256: return launch_fwd16_dt<256, 1>(p, s);
+    case 64: return launch_fwd16_default_d64(p, s, cta_pairs);
+    case 128: return launch_fwd16_default_d128(p, s, cta_pairs);
+    case 256: return launch_fwd16_default_d256(p, s, false);
   }
   return FA3B_ERR_HEAD_DIM;
 }

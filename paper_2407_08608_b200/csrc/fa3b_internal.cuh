@@ -20,6 +20,14 @@ int validate_problem(int batch, int heads_q, int heads_kv, int seqlen, int head_
                      double alpha);
 
 int launch_fwd_fp8(const fa3b_fwd_params& p, cudaStream_t stream);
+// f16/bf16 forward launchers, one translation unit each (fwd16_*.cu)
+int launch_fwd16_default_d64(const fa3b_fwd_params& p, cudaStream_t s, bool cta_pairs);
+int launch_fwd16_default_d128(const fa3b_fwd_params& p, cudaStream_t s, bool cta_pairs);
+int launch_fwd16_default_d256(const fa3b_fwd_params& p, cudaStream_t s, bool cta_pairs);
+int launch_fwd16_sched_bf16_c0(const fa3b_fwd_params& p, cudaStream_t s);
+int launch_fwd16_sched_bf16_c1(const fa3b_fwd_params& p, cudaStream_t s);
+int launch_fwd16_sched_f16_c0(const fa3b_fwd_params& p, cudaStream_t s);
+int launch_fwd16_sched_f16_c1(const fa3b_fwd_params& p, cudaStream_t s);
 // Raise a kernel's dynamic shared-memory limit once per (kernel, device): the
 // attribute belongs to the function as loaded on the current device, so a
 // process driving several GPUs needs it on each.

@@ -133,20 +133,41 @@ struct FwdArgs {
   const float* v_scale;
   int q_blocked, kv_blocked;
   float fp8_thr;         // lazy-rescale threshold (log2) for the e4m3 P
-  float fp8_pmul, fp8_inv_pmul, fp8_lpm;  // 448 / 2^thr, its inverse and log2 (host-computed)
+  float fp8_pmul, fp8_inv_pmul, fp8_lpm;  // P code scale, its inverse and log2 (host-computed):
+                                          // 448 / 2^thr, or 224 / 2^thr with per-block V
+                                          // scales (headroom for the folded V ratio)
 };
 __device__ __forceinline__ int fwd_seqlen(const FwdArgs& a) { return a.N; }
 
 
+// Kernel schedule variants (include/fa3b.h fa3b_schedule). SCHED_DEFAULT is the
+// production path; the others exist for the reference's three schedules and the
+// paper's ablation and only apply to one-tile CTAs (NT = 1).
+enum FwdSched {
+  SCHED_DEFAULT = 0,  // NT = 2 ping-pong (S3 at d = 64) or, with NT = 1, S2 = 3-stage
+  SCHED_SERIAL = 1,   // one S buffer: S_j -> softmax_j -> PV_j strictly in sequence
+  SCHED_3STAGE = 2,   // = the NT = 1 S2 path (softmax_j overlaps S_{j+1} and PV_{j-1})
+  SCHED_2STAGE = 3,   // S2, but softmax_j starts only after PV_{j-1} has completed
+  SCHED_NOWS = 4      // S2 pipelining issued by the softmax warps (no producer / MMA warps)
+};
+
 // CPS_ = CTAs per SM. CPS = 2 (one query tile per CTA, d <= 128) gives the
 // tensor core two independent tiles per SM from two CTAs instead of one CTA's
 // ping-pong pair: half the TMEM (256 columns) and fewer K/V stages each.
-template <int D_, int NT_, int EB_ = 2, int CPS_ = 1>
+// NQ_ = column splits of a query tile over its softmax warpgroups: 2 (two
+// warpgroups, 64 S columns per thread) or 4 (four warpgroups, 32 columns per
+// thread: half the per-thread softmax chain, for the one-tile S2 schedule).
+template <int D_, int NT_, int EB_ = 2, int CPS_ = 1, int SCHED_ = SCHED_DEFAULT, int NQ_ = 2>
 struct FwdTraits {
   static constexpr int D = D_;
   static constexpr int NT = NT_;
+  static constexpr int NQ = NQ_;
+  static_assert(NQ == 2 || (NQ == 4 && NT_ == 1 && CPS_ == 1 && SCHED_ != SCHED_NOWS), "NQ = 4 is one-tile");
+  static constexpr int WPT = 4 * NQ;  // softmax warps per query tile
   static constexpr int EB = EB_;  // bytes per element (2 f16/bf16, 1 e4m3)
   static constexpr int CPS = CPS_;
+  static constexpr int SCHED = SCHED_;
+  static_assert(SCHED == SCHED_DEFAULT || (NT == 1 && CPS == 1), "schedule variants are one-tile");
   static constexpr int BM = 128;
   static constexpr int BN = 128;
   static constexpr int CHUNK_BYTES = 128 * 128;  // 128 rows x 128 bytes
@@ -155,14 +176,20 @@ struct FwdTraits {
   static constexpr int TILE_BYTES = CHUNKS * CHUNK_BYTES;
   static constexpr int STAGES = CPS == 2 ? (TILE_BYTES <= 16384 ? 4 : 2)
                                          : (TILE_BYTES <= 16384 ? 8 : (TILE_BYTES <= 32768 ? 4 : 2));
+  // no warp specialization: the softmax warps issue loads and MMAs themselves
+  static constexpr bool NOWS = SCHED == SCHED_NOWS;
+  static_assert(!NOWS || STAGES >= 4, "no-WS schedule needs a 4-stage K/V ring");
   // two softmax warpgroups per query tile, each owning 64 of the 128 columns
   static constexpr int SOFT_REGS = (CPS == 1 && NT == 2) ? FA3B_FWD_REGS : 0;
-  static constexpr int NUM_THREADS = NT * 256 + (SOFT_REGS > 0 ? 128 : 64);
-  static constexpr int LOAD_WARP = NT * 8;
-  static constexpr int MMA_WARP = NT * 8 + 1;
+  static constexpr int NSOFT = NT * WPT;  // softmax warps
+  static constexpr int NUM_THREADS = NOWS ? NSOFT * 32 : NSOFT * 32 + (SOFT_REGS > 0 ? 128 : 64);
+  static constexpr int LOAD_WARP = NOWS ? -1 : NSOFT;
+  static constexpr int MMA_WARP = NOWS ? -1 : NSOFT + 1;
+  static constexpr int ALLOC_WARP = NOWS ? 0 : NSOFT + 1;  // barrier init, TMEM alloc / free
   static constexpr uint32_t TMEM_COLS = CPS == 2 ? 256 : 512;
   // one query tile per CTA: a second S buffer after O (see the header)
-  static constexpr bool S2 = NT == 1 && CPS == 1 && FA3B_FWD_S2;
+  static constexpr bool S2 = NT == 1 && CPS == 1 && FA3B_FWD_S2 && SCHED != SCHED_SERIAL;
+  static constexpr bool TWO_STAGE = SCHED == SCHED_2STAGE;
   static_assert(!S2 || 2 * 128 + D <= 512, "S2 TMEM budget");
   // d = 64 tile pair: three S buffers rotate between the two tiles (3 x 128 + 2 x 64
   // columns), so each tile's next S is computed during its softmax (see the header)
@@ -174,9 +201,9 @@ struct FwdTraits {
   // q_full, kv_full[S], kv_empty[S], s_full[2 NT], p_full[NT], o_full[NT], q_empty,
   // pv_done[NT] (the second s_full per tile and pv_done serve S2 / S3)
   static constexpr int NUM_BARS = 3 + 2 * STAGES + 5 * NT;
-  // row-max / row-sum exchange between the two column halves: [NT][2 buf][2 half][128]
+  // row-max / row-sum exchange between the column splits: [NT][2 buf][NQ][128]
   static constexpr int OFF_XCH = OFF_BAR + NUM_BARS * 8 + 16;
-  static constexpr int SMEM_BYTES = OFF_XCH + NT * 2 * 2 * 128 * 4 + 1024;
+  static constexpr int SMEM_BYTES = OFF_XCH + NT * 2 * NQ * 128 * 4 + 1024;
   static_assert(NT * (128 + D) <= static_cast<int>(TMEM_COLS), "TMEM budget");
   static_assert(CPS == 1 || (NT == 1 && SMEM_BYTES * 2 <= 233472), "two CTAs per SM");
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
@@ -185,20 +212,154 @@ struct FwdTraits {
   __host__ __device__ static constexpr int o_col(int t) { return (S3 ? 384 : NT * 128) + t * D; }
 };
 
+// SCHED_NOWS: the producer and MMA-issuer work of the one-tile S2 schedule, done
+// by thread 0 of the softmax warps between its own softmax iterations. K/V go
+// through the ring in the S2 order K_0, K_1, {V_j, K_{j+2}}; a load is issued
+// only once its slot's previous occupant was consumed by an MMA issued at least
+// one iteration earlier (at most STAGES - 2 entries ahead), so the leader's
+// kv_empty waits are short; the MMAs follow S_0 ; S_1 ; {PV_j ; S_{j+2}}.
+template <class T, bool FP8>
+struct NowsLeader {
+  uint8_t* smem;
+  uint32_t tmem, q_addr, kv_addr;
+  const CUtensorMap *tmQ, *tmK, *tmV;
+  uint64_t *q_full, *kv_full, *kv_empty, *s_full, *p_full, *o_full, *pv_done;
+  uint32_t idesc_qk, idesc_pv;
+  int lpos = 0;   // ring loads issued (all items)
+  int cpos = 0;   // ring entries consumed by issued MMAs (all items)
+  int gs = 0;     // S GEMMs issued (buffer gs & 1)
+  int pc = 0;     // p_full phases consumed
+  int g0 = 0;     // gs at this item's S_0
+  int it_h = 0, it_hkv = 0, it_b = 0, it_n = 0;
+  int k_next = 0, v_next = 0, l_item = 0;  // this item's load sequence
+  bool v_turn = true;
+  __device__ NowsLeader(uint8_t* sm, uint32_t tm, const CUtensorMap* q, const CUtensorMap* k,
+                        const CUtensorMap* v, uint64_t* bars, uint32_t iqk, uint32_t ipv)
+      : smem(sm), tmem(tm), tmQ(q), tmK(k), tmV(v), idesc_qk(iqk), idesc_pv(ipv) {
+    q_addr = ptx::smem_u32(smem + T::OFF_Q);
+    kv_addr = ptx::smem_u32(smem + T::OFF_KV);
+    q_full = bars;
+    kv_full = bars + 1;
+    kv_empty = kv_full + T::STAGES;
+    s_full = kv_empty + T::STAGES;
+    p_full = s_full + 2;
+    o_full = p_full + 1;
+    pv_done = o_full + 2;
+  }
+  // issue the item's next loads while their slots were freed an iteration ago
+  __device__ void loads() {
+    while (l_item < 2 * it_n && lpos < cpos - 2 + T::STAGES) {
+      bool is_v;
+      int blk;
+      if (k_next < 2 && k_next < it_n) {
+        is_v = false;
+        blk = k_next++;
+      } else if (v_next < it_n && (v_turn || k_next >= it_n)) {
+        is_v = true;
+        blk = v_next++;
+        v_turn = false;
+      } else {
+        is_v = false;
+        blk = k_next++;
+        v_turn = true;
+      }
+      const int slot = lpos % T::STAGES;
+      ptx::mbar_wait(&kv_empty[slot], ((lpos / T::STAGES) & 1) ^ 1);
+      ptx::mbar_arrive_expect_tx(&kv_full[slot], T::TILE_BYTES);
+#pragma unroll
+      for (int c = 0; c < T::CHUNKS; ++c)
+        ptx::tma_load_4d(smem + T::OFF_KV + slot * T::TILE_BYTES + c * T::CHUNK_BYTES,
+                         is_v ? tmV : tmK, &kv_full[slot], c * T::CHUNK_ELEMS, it_hkv, blk * 128,
+                         it_b, ptx::kEvictLast);
+      ++lpos;
+      ++l_item;
+    }
+  }
+  __device__ int wait_next() {
+    const int slot = cpos % T::STAGES;
+    ptx::mbar_wait(&kv_full[slot], (cpos / T::STAGES) & 1);
+    ptx::tc_fence_after();
+    ++cpos;
+    return slot;
+  }
+  __device__ void s_issue() {
+    const int slot = wait_next();
+    constexpr int KSTEP = 32 / T::EB;
+#pragma unroll
+    for (int k = 0; k < T::D / KSTEP; ++k) {
+      const uint32_t off = (k >> 2) * T::CHUNK_BYTES + (k & 3) * 32;
+      const uint64_t a = ptx::sw128_desc(q_addr + off, 16, 1024);
+      const uint64_t bd = ptx::sw128_desc(kv_addr + slot * T::TILE_BYTES + off, 16, 1024);
+      if constexpr (FP8)
+        ptx::mma_f8_ss(tmem + T::s2_col(gs & 1), a, bd, idesc_qk, k > 0 ? 1u : 0u);
+      else
+        ptx::mma_f16_ss(tmem + T::s2_col(gs & 1), a, bd, idesc_qk, k > 0 ? 1u : 0u);
+    }
+    ptx::mma_commit(&s_full[gs & 1]);
+    ptx::mma_commit(&kv_empty[slot]);
+    ++gs;
+  }
+  __device__ void item_start(int h, int hkv, int b, int q_base, int n, int itl) {
+    it_h = h;
+    it_hkv = hkv;
+    it_b = b;
+    it_n = n;
+    k_next = v_next = l_item = 0;
+    v_turn = true;
+    g0 = gs;
+    if (n == 0) return;
+    // Q: every MMA of the previous item has completed (its epilogue waited o_full)
+    ptx::mbar_arrive_expect_tx(q_full, T::TILE_BYTES);
+#pragma unroll
+    for (int c = 0; c < T::CHUNKS; ++c)
+      ptx::tma_load_4d(smem + T::OFF_Q + c * T::CHUNK_BYTES, tmQ, q_full, c * T::CHUNK_ELEMS, h,
+                       q_base, b, ptx::kEvictFirst);
+    loads();
+    ptx::mbar_wait(q_full, itl & 1);
+    for (int j = 0; j < 2 && j < n; ++j) s_issue();
+    loads();
+  }
+  // after this thread's own P_j store: wait for every softmax warp, then PV_j and S_{j+2}
+  __device__ void after_p(int j, int n) {
+    ptx::mbar_wait(p_full, pc++ & 1);
+    ptx::tc_fence_after();
+    const int slot = wait_next();
+    constexpr int KSTEP = 32 / T::EB;
+    const uint32_t scol = T::s2_col((g0 + j) & 1);
+#pragma unroll
+    for (int k = 0; k < 128 / KSTEP; ++k) {
+      const uint64_t bd = ptx::sw128_desc(kv_addr + slot * T::TILE_BYTES + k * KSTEP * 128,
+                                          T::CHUNK_BYTES, 1024);
+      if constexpr (FP8)
+        ptx::mma_f8_ts(tmem + T::o_col(0), tmem + scol + k * 8, bd, idesc_pv,
+                       (j > 0 || k > 0) ? 1u : 0u);
+      else
+        ptx::mma_f16_ts(tmem + T::o_col(0), tmem + scol + k * 8, bd, idesc_pv,
+                        (j > 0 || k > 0) ? 1u : 0u);
+    }
+    ptx::mma_commit(pv_done);
+    ptx::mma_commit(&kv_empty[slot]);
+    if (j + 1 == n) ptx::mma_commit(o_full);
+    if (j + 2 < n) s_issue();
+    loads();
+  }
+};
+
 // EMU: how many of every 8 exp2 pairs run on the FMA-pipe polynomial.
 #ifndef FA3B_FWD_EMU
 #define FA3B_FWD_EMU 2
 #endif
 
-template <int D, int NT, bool CAUSAL, int KIND, int CPS = 1, int EMU = FA3B_FWD_EMU>
-__global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CPS>::NUM_THREADS, CPS)
+template <int D, int NT, bool CAUSAL, int KIND, int CPS = 1, int EMU = FA3B_FWD_EMU,
+          int SCHED = SCHED_DEFAULT, int NQ = 2>
+__global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CPS, SCHED, NQ>::NUM_THREADS, CPS)
     fa3b_fwd_kernel(const __grid_constant__ CUtensorMap tmQ,
                     const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const FwdArgs args,
                     const uint32_t idesc_qk, const uint32_t idesc_pv) {
   constexpr bool FP8 = KIND == KIND_E4M3;
   constexpr bool BF16 = KIND == KIND_BF16;
-  using T = FwdTraits<D, NT, FP8 ? 1 : 2, CPS>;
+  using T = FwdTraits<D, NT, FP8 ? 1 : 2, CPS, SCHED, NQ>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -260,7 +421,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
     return w;
   };
 
-  if (warp == T::MMA_WARP) {
+  if (warp == T::ALLOC_WARP) {
     if (ptx::lane_id() == 0) {
       ptx::mbar_init(q_full, 1);
       for (int s = 0; s < T::STAGES; ++s) {
@@ -271,7 +432,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
         ptx::mbar_init(&s_full[2 * t], 1);
         ptx::mbar_init(&s_full[2 * t + 1], 1);
         ptx::mbar_init(&pv_done[t], 1);
-        ptx::mbar_init(&p_full[t], 8);  // one arrival per softmax warp
+        ptx::mbar_init(&p_full[t], T::WPT);  // one arrival per softmax warp
         ptx::mbar_init(&o_full[t], 1);
       }
       ptx::mbar_init(q_empty, 1);
@@ -280,7 +441,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
     __syncwarp();
     ptx::tmem_alloc<T::TMEM_COLS>(tmem_slot);
   }
-  if (warp == T::LOAD_WARP && ptx::lane_id() == 0) {
+  if (warp == (T::NOWS ? 0 : T::LOAD_WARP) && ptx::lane_id() == 0) {
     ptx::prefetch_tmap(&tmQ);
     ptx::prefetch_tmap(&tmK);
     ptx::prefetch_tmap(&tmV);
@@ -294,7 +455,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
 
   if constexpr (T::SOFT_REGS > 0) {
     static_assert(NT * 8 * T::SOFT_REGS + 4 * FA3B_FWD_OREGS <= (T::NUM_THREADS / 32) * 96, "register pool");
-    if (warp >= NT * 8)
+    if (warp >= T::NSOFT)
       ptx::setmaxnreg_dec<FA3B_FWD_OREGS>();
   }
   if (warp == T::LOAD_WARP) {
@@ -578,28 +739,41 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
         kvi += 2 * w.n_max;
       }
     }
-  } else if (warp < NT * 8) {
+  } else if (warp < T::NSOFT) {
     // ------------------------------------------------------------ softmax
     if constexpr (T::SOFT_REGS > 0) ptx::setmaxnreg_inc<T::SOFT_REGS>();
     const uint32_t tmem = FA3B_TMEM_BASE;
-    const int t = warp >> 3;             // query tile
-    const int hh = (warp >> 2) & 1;      // column half of S / O
+    const int t = warp / T::WPT;         // query tile
+    const int hh = (warp >> 2) % NQ;     // column split of S / O
     const int r = ((warp & 3) << 5) | static_cast<int>(ptx::lane_id());  // row == TMEM lane
     const uint32_t lane_base = static_cast<uint32_t>(32 * (warp & 3)) << 16;
     const uint32_t tS0 = tmem + lane_base + T::s_col(t);
     const uint32_t tO = tmem + lane_base + T::o_col(t);
-    float* xch = reinterpret_cast<float*>(smem + T::OFF_XCH) + t * 512;  // [2 buf][2 half][128]
+    float* xch = reinterpret_cast<float*>(smem + T::OFF_XCH) + t * (2 * NQ * 128);  // [2 buf][NQ][128]
     const uint32_t bar_id = 1 + t;
     int sc = 0, xc = 0, oc = 0;  // s_full / exchange-buffer / o_full uses so far
     int gbase = 0;               // S3: 2 x (KV blocks of this CTA's previous items)
     int itl = 0;
+    // no warp specialization (SCHED_NOWS): thread 0 of the softmax warps is also the
+    // TMA producer and the MMA issuer, at fixed points of its own softmax loop
+    const bool leader = T::NOWS && threadIdx.x == 0;
+    NowsLeader<T, FP8> nows(smem, tmem, &tmQ, &tmK, &tmV, bars, idesc_qk, idesc_pv);
     for (int lin = item_of(0); lin < num_items; lin = item_of(++itl)) {
     const Item w = decode(lin);
     const int b = w.b, h = w.h, hkv = w.hkv, q_base = w.q_base;
     const int q_row = q_base + t * 128 + r;
+    if constexpr (T::NOWS)
+      if (leader) nows.item_start(w.h, w.hkv, w.b, w.q_base, w.n_t[0], itl);
     const int nt = (t == 0) ? w.n_t[0] : w.n_t[NT - 1];
-    constexpr int HC = 64;               // columns per half
-    constexpr int DH = D / 2;            // O columns per half
+    constexpr int HC = 128 / NQ;         // S columns per thread
+    constexpr int DH = D / NQ;           // O columns per thread
+    constexpr int CW = DH < 32 ? DH : 32;  // O columns per TMEM load / store
+    auto tmem_ldw = [](uint32_t a, uint32_t (&v)[CW]) {
+      if constexpr (CW == 32) ptx::tmem_ld32(a, v); else ptx::tmem_ld16(a, v);
+    };
+    auto tmem_stw = [](uint32_t a, const uint32_t (&v)[CW]) {
+      if constexpr (CW == 32) ptx::tmem_st32(a, v); else ptx::tmem_st16(a, v);
+    };
     float sl2 = args.scale_log2;
     const float thr = FP8 ? args.fp8_thr : 8.f;
     float out_scale = 1.f;
@@ -630,6 +804,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
     for (int j = 0; j < nt; ++j) {
       float slj = sl2;
       float vfac = 1.f;  // O rescale for a new V block scale (uniform across the CTA)
+      float lrho = 0.f, inv_rho = 1.f;  // FP8: V-scale ratio folded into this block's P
       if constexpr (FP8) {
         slj = sl2 * ks_next;
         const float vs = vs_next;
@@ -638,12 +813,24 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
           vs_next = args.v_scale[ks_base + j + 1];
         }
         if (vs != v_cur) {
-          vfac = v_cur / vs;  // 0 on the first block: O is empty
-          v_cur = vs;
+          // O stays in units of v_cur while rho = s_v[j] / v_cur is in [1/2, 2): the
+          // ratio scales this block's P codes instead (the P scale keeps one bit of
+          // headroom for it), so O is rescaled only when rho leaves that range
+          const float rho = vs / v_cur;  // inf on the first block (v_cur = 0)
+          if (rho >= 0.5f && rho < 2.f) {
+            lrho = __log2f(rho);
+            inv_rho = v_cur / vs;
+          } else {
+            vfac = v_cur / vs;  // 0 on the first block: O is empty
+            v_cur = vs;
+          }
         }
       }
-      const bool tr = itl == 0 && (warp & 7) == 0 && ptx::lane_id() == 0;
+      const bool tr = itl == 0 && (warp % T::WPT) == 0 && ptx::lane_id() == 0;
       if (tr) FA3B_TP(t, j, 0);
+      // 2-stage order (flash_fwd.cpp:148-169): softmax_j begins once PV_{j-1} is done
+      if constexpr (T::TWO_STAGE)
+        if (j > 0) ptx::mbar_wait(&pv_done[t], (sc - 1) & 1);
       if constexpr (T::S2 || T::S3)
         ptx::mbar_wait(&s_full[2 * t + (sc & 1)], (sc >> 1) & 1);
       else
@@ -664,8 +851,9 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       const bool need_mask = (j * 128 + 128 > N) || (CAUSAL && j == nt - 1);
       auto load_s = [&]() {
         uint32_t sr[HC];
-        ptx::tmem_ld32(tS + HC * hh, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-        ptx::tmem_ld32(tS + HC * hh + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+#pragma unroll
+        for (int c = 0; c < HC / 32; ++c)
+          ptx::tmem_ld32(tS + HC * hh + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(&sr[32 * c]));
         ptx::tmem_wait_ld();
 #pragma unroll
         for (int i = 0; i < HC; ++i) s[i] = __uint_as_float(sr[i]);
@@ -677,28 +865,30 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       };
       load_s();
       if (tr) FA3B_TP(t, j, 2);
-      // half-row max: FMNMX3 over 4 independent chains, then swap with the other half
+      // partial row max: FMNMX3 over 4 independent chains, then exchange with the
+      // other column splits of the row
       float a0 = s[0], a1 = s[1], a2 = s[2], a3 = s[3];
 #pragma unroll
-      for (int i = 4; i < 60; i += 8) {
+      for (int i = 4; i + 8 <= HC; i += 8) {
         a0 = ptx::max3(a0, s[i], s[i + 1]);
         a1 = ptx::max3(a1, s[i + 2], s[i + 3]);
         a2 = ptx::max3(a2, s[i + 4], s[i + 5]);
         a3 = ptx::max3(a3, s[i + 6], s[i + 7]);
       }
-      a0 = ptx::max3(a0, s[60], s[61]);
-      a1 = ptx::max3(a1, s[62], s[63]);
+      a0 = ptx::max3(a0, s[HC - 4], s[HC - 3]);
+      a1 = ptx::max3(a1, s[HC - 2], s[HC - 1]);
       const float pm = fmaxf(ptx::max3(a0, a1, a2), a3);
-      float* xb = xch + (xc & 1) * 256;
+      float* xb = xch + (xc & 1) * (NQ * 128);
       ++xc;
       ptx::sts_f32(xb + hh * 128 + r, pm);
       // P = 2^(s * slj - msub) for this half: FFMA2 pairs; EMU of every 8 pairs go
       // through the FMA-pipe polynomial, the rest through MUFU.EX2; FADD2 sums.
-      constexpr int NPK = FP8 ? 16 : 32;
+      constexpr int NPK = FP8 ? HC / 4 : HC / 2;
       uint32_t pk[NPK];
       float psum = 0.f;
       auto exp_half = [&](float msub) {
-        const float2 sc2 = make_float2(slj, slj), nm2 = make_float2(lpm - msub, lpm - msub);
+        const float2 sc2 = make_float2(slj, slj),
+                     nm2 = make_float2(lpm + lrho - msub, lpm + lrho - msub);
         float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                          make_float2(0.f, 0.f)};
         float2 prev = make_float2(0.f, 0.f);
@@ -725,41 +915,48 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
         const float2 a4 = __fadd2_rn(__fadd2_rn(acc[0], acc[1]), __fadd2_rn(acc[2], acc[3]));
         psum = a4.x + a4.y;
       };
-      ptx::named_bar_sync(bar_id, 256);  // also: every S load of this tile has completed
-      const float mx = fmaxf(pm, ptx::lds_f32(xb + (hh ^ 1) * 128 + r));
+      ptx::named_bar_sync(bar_id, NQ * 128);  // also: every S load of this tile has completed
+      float mx = pm;
+#pragma unroll
+      for (int q = 1; q < NQ; ++q) mx = fmaxf(mx, ptx::lds_f32(xb + ((hh + q) % NQ) * 128 + r));
       if (tr) FA3B_TP(t, j, 3);
       const float m_new = fmaxf(m_use, mx * slj);
       const bool resc = m_new > m_use + thr;
       const float m_cur = resc ? m_new : m_use;
       const float factor = resc ? ptx::ex2(m_use - m_new) : 1.f;
       exp_half((m_cur == -INFINITY) ? 0.f : m_cur);
-      if constexpr (FP8)
-        ptx::tmem_st16(tS + 16 * hh, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
+      // P (packed, key order) over the first columns of this block's S buffer; every
+      // split's S load has completed (the exchange barrier above)
+      if constexpr (NPK == 8)
+        ptx::tmem_st8(tS + NPK * hh, *reinterpret_cast<uint32_t(*)[8]>(&pk[0]));
+      else if constexpr (NPK == 16)
+        ptx::tmem_st16(tS + NPK * hh, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
       else
-        ptx::tmem_st32(tS + 32 * hh, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
-      l = l * factor + psum * inv_pmul;
+        ptx::tmem_st32(tS + NPK * hh, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+      l = l * factor + psum * (inv_pmul * inv_rho);
       if (tr) FA3B_TP(t, j, 4);
       const float ofac = factor * vfac;
       // S2: every iteration waits for PV(V_{j-1}) before handing over P_j, so one
       // PV is in flight at a time and the pv_done parity never skips a phase (a
       // wait only when O needs rescaling hung at bf16 d = 256)
-      if constexpr (T::S2 || T::S3)
+      if constexpr ((T::S2 || T::S3) && !T::TWO_STAGE)
         if (j > 0) ptx::mbar_wait(&pv_done[t], (sc - 2) & 1);
       if (j > 0 && __any_sync(0xffffffffu, ofac != 1.f)) {
-        // PV(V_{j-1}) is complete (see header / above); rescale this half-row of O_t.
-        constexpr int G = DH / 32 < 4 ? DH / 32 : 4;
+        // PV(V_{j-1}) is complete (see header / above); rescale this thread's O_t columns.
+        constexpr int NC = DH / CW;
+        constexpr int G = NC < 4 ? NC : 4;
 #pragma unroll
-        for (int c0 = 0; c0 < DH / 32; c0 += G) {
-          uint32_t ov[G][32];
+        for (int c0 = 0; c0 < NC; c0 += G) {
+          uint32_t ov[G][CW];
 #pragma unroll
-          for (int c = 0; c < G; ++c) ptx::tmem_ld32(tO + DH * hh + (c0 + c) * 32, ov[c]);
+          for (int c = 0; c < G; ++c) tmem_ldw(tO + DH * hh + (c0 + c) * CW, ov[c]);
           ptx::tmem_wait_ld();
 #pragma unroll
           for (int c = 0; c < G; ++c) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
+            for (int i = 0; i < CW; ++i)
               ov[c][i] = __float_as_uint(__uint_as_float(ov[c][i]) * ofac);
-            ptx::tmem_st32(tO + DH * hh + (c0 + c) * 32, ov[c]);
+            tmem_stw(tO + DH * hh + (c0 + c) * CW, ov[c]);
           }
         }
       }
@@ -769,48 +966,56 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       if (tr) FA3B_TP(t, j, 5);
       if (ptx::lane_id() == 0) ptx::mbar_arrive(&p_full[t]);  // one arrival per warp
       m_use = m_cur;
+      if constexpr (T::NOWS)
+        if (leader) nows.after_p(j, nt);
     }
     if (nt > 0) {
       // ---------------------------------------------------------- epilogue
-      float* xb = xch + (xc & 1) * 256;
+      float* xb = xch + (xc & 1) * (NQ * 128);
       ++xc;
       ptx::sts_f32(xb + hh * 128 + r, l);
-      ptx::named_bar_sync(bar_id, 256);
-      l += ptx::lds_f32(xb + (hh ^ 1) * 128 + r);
+      ptx::named_bar_sync(bar_id, NQ * 128);
+      {
+        // the row sum in a fixed order of the splits (the same in every thread of the row)
+        float lt = 0.f;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) lt += q == hh ? l : ptx::lds_f32(xb + q * 128 + r);
+        l = lt;
+      }
       ptx::mbar_wait(&o_full[t], oc & 1);
       ++oc;
       ptx::tc_fence_after();
-      if constexpr (FP8) out_scale = v_cur * ptx::ex2(thr) * (1.f / 448.f);
+      if constexpr (FP8) out_scale = v_cur * inv_pmul;
       const float inv = l > 0.f ? out_scale / l : 0.f;
       const bool row_ok = q_row < N;
       const size_t obase = static_cast<size_t>(b) * args.o_sb +
                            static_cast<size_t>(q_row) * args.o_ss +
                            static_cast<size_t>(h) * args.o_sh + DH * hh;
 #pragma unroll
-      for (int c = 0; c < DH / 32; ++c) {
-        uint32_t ov[32];
-        ptx::tmem_ld32(tO + DH * hh + c * 32, ov);
+      for (int c = 0; c < DH / CW; ++c) {
+        uint32_t ov[CW];
+        tmem_ldw(tO + DH * hh + c * CW, ov);
         ptx::tmem_wait_ld();
         if (!row_ok) continue;
         if (args.out_f32) {
-          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(args.o) + obase + c * 32);
+          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(args.o) + obase + c * CW);
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
+          for (int i = 0; i < CW / 4; ++i)
             dst[i] = make_float4(__uint_as_float(ov[4 * i]) * inv,
                                  __uint_as_float(ov[4 * i + 1]) * inv,
                                  __uint_as_float(ov[4 * i + 2]) * inv,
                                  __uint_as_float(ov[4 * i + 3]) * inv);
         } else {
-          uint32_t pk[16];
+          uint32_t pk[CW / 2];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
+          for (int i = 0; i < CW / 2; ++i) {
             const float a = __uint_as_float(ov[2 * i]) * inv;
             const float bb = __uint_as_float(ov[2 * i + 1]) * inv;
             pk[i] = (BF16 || FP8) ? ptx::pack_bf16(a, bb) : ptx::pack_f16(a, bb);
           }
-          uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(args.o) + obase + c * 32);
+          uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(args.o) + obase + c * CW);
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
+          for (int i = 0; i < CW / 8; ++i)
             dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
         }
       }
@@ -828,7 +1033,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
 #ifdef FA3B_TRACE
   if (threadIdx.x == 0) FA3B_CTA(2, fa3b_gtime());
 #endif
-  if (warp == T::MMA_WARP) {
+  if (warp == T::ALLOC_WARP) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<T::TMEM_COLS>(FA3B_TMEM_BASE);
   }

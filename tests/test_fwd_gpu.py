@@ -63,8 +63,13 @@ CASES = [
     pytest.param(2, 2, 2, 130, 64, True, "fp16", "pingpong", 0.3, id="tile1-partial"),
     pytest.param(1, 2, 2, 100, 64, False, "bf16", "pingpong", None, id="N-lt-128"),
     pytest.param(1, 1, 1, 1, 64, False, "bf16", "pingpong", None, id="N1"),
-    pytest.param(1, 2, 2, 640, 128, True, "fp16", "3stage", None, id="3stage-alias"),
-    pytest.param(1, 2, 2, 512, 256, False, "fp16", "basic", 0.02, id="d256-fp16"),
+    pytest.param(1, 2, 2, 640, 128, True, "fp16", "3stage", None, id="3stage-d128"),
+    pytest.param(1, 2, 2, 512, 256, False, "fp16", "basic", 0.02, id="d256-fp16-serial"),
+    pytest.param(1, 2, 1, 700, 64, True, "bf16", "2stage", None, id="2stage-d64-gqa"),
+    pytest.param(1, 2, 2, 513, 256, True, "bf16", "2stage", None, id="2stage-d256"),
+    pytest.param(2, 2, 2, 1000, 128, False, "fp16", "no_ws", None, id="nows-d128"),
+    pytest.param(1, 4, 2, 300, 64, True, "bf16", "no_ws", -0.2, id="nows-d64-causal"),
+    pytest.param(1, 2, 2, 257, 128, True, "bf16", "basic", None, id="serial-d128"),
 ]
 
 
@@ -127,18 +132,54 @@ def test_gqa_mapping_equals_duplication_bitwise(port, cuda):
         assert torch.equal(o1, o2) and torch.equal(l1, l2)
 
 
-def test_schedules_and_reruns_bit_identical(port, cuda):
+SCHEDULES = ("pingpong", "basic", "3stage", "2stage", "no_ws")
+
+
+@pytest.mark.parametrize("D", [64, 128, 256])
+def test_schedules_and_reruns_bit_identical(port, cuda, D):
     """The reference demands bit-identical schedules (test_flash_fwd.cpp:152-196)
-    and deterministic reruns; the device kernels keep both."""
+    and deterministic reruns; every device schedule (ping-pong, serial basic,
+    3-stage, 2-stage, no warp specialization) runs the same per-tile arithmetic
+    in another order, so all agree bitwise in 16-bit."""
     api = _api()
     torch = _torch()
+    from paper_2407_08608_b200._lib import Fa3bError
     for causal in (False, True):
-        q, k, v = (to_dev(x, torch.bfloat16) for x in make_inputs(port, 1, 2, 2, 700, 128, 9))
+        q, k, v = (to_dev(x, torch.bfloat16) for x in make_inputs(port, 1, 2, 2, 700, D, 9))
         a = api.fwd(q, k, v, causal=causal, schedule="pingpong")
-        b = api.fwd(q, k, v, causal=causal, schedule="basic")
         c = api.fwd(q, k, v, causal=causal, schedule="pingpong")
         assert torch.equal(a[0], c[0]) and torch.equal(a[1], c[1])
-        assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+        for sched in SCHEDULES[1:]:
+            if D == 256 and sched == "no_ws":
+                with pytest.raises(Fa3bError, match="schedule"):
+                    api.fwd(q, k, v, causal=causal, schedule=sched)
+                continue
+            b = api.fwd(q, k, v, causal=causal, schedule=sched)
+            assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1]), sched
+
+
+@pytest.mark.parametrize("sched", ["basic", "2stage", "3stage", "no_ws"])
+def test_schedule_variants_many_items(cuda, sched):
+    """The one-tile variants over many persistent work items (several rounds of the
+    148-CTA grid, ragged last block, GQA): sampled rows against fp32 torch."""
+    api = _api()
+    torch = _torch()
+    B, N, H, Hkv, D = 2, 4100, 24, 8, 128
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    q = torch.randn(B, N, H, D, device="cuda", generator=gen, dtype=torch.bfloat16)
+    k, v = (torch.randn(B, N, Hkv, D, device="cuda", generator=gen, dtype=torch.bfloat16)
+            for _ in range(2))
+    for causal in (False, True):
+        o, lse = api.fwd(q, k, v, causal=causal, schedule=sched)
+        o_ref, lse_ref = api.fwd(q, k, v, causal=causal)
+        assert torch.equal(o, o_ref) and torch.equal(lse, lse_ref)
+        rows = torch.tensor([0, 1, 127, 128, 2049, N - 1], device="cuda")
+        for b, h in ((0, 0), (1, 23)):
+            s = q[b, rows, h].float() @ k[b, :, h // 3].float().T / math.sqrt(D)
+            if causal:
+                s = s.masked_fill(torch.arange(N, device="cuda")[None, :] > rows[:, None], -math.inf)
+            ref = torch.softmax(s, -1) @ v[b, :, h // 3].float()
+            assert (o[b, rows, h].float() - ref).abs().max().item() < 2e-2
 
 
 def test_strided_inputs(port, cuda):
