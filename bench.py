@@ -269,8 +269,10 @@ def fp8_peak_tflops(torch, dev):
 
 
 def _prep3(api, x, stream, seed=1):
-    """K5 on Q, K (Hadamard, per-block scales) and V (per-block scales)."""
-    return [api.fp8_prepare(t, block_rows=128, hadamard=i < 2, seed=seed, stream=stream)
+    """K5 on Q, K (Hadamard, per-block scales) and V (per-block power-of-two
+    scales), as api.fp8_fwd does."""
+    return [api.fp8_prepare(t, block_rows=128, hadamard=i < 2, seed=seed, scale_pow2=i == 2,
+                            stream=stream)
             for i, t in enumerate(x)]
 
 

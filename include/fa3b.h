@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define FA3B_ABI_VERSION 1
+#define FA3B_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define FA3B_API __attribute__((visibility("default")))
@@ -152,6 +152,11 @@ typedef struct fa3b_fp8_prepare_params {
   uint64_t seed;        /* sign vector seed: sign_i = +1 iff word(i) is odd */
   int32_t saturate;     /* 1: clamp |code| to 448 (reference default); 0: overflow to NaN */
   void* stream;
+  /* Added in ABI 2 (an ABI 1 struct_size, without it, reads as 0). 1: scale = the smallest
+     power of two >= amax / 448 (codes of a block's maximum land in (224, 448]).
+     Not a reference mode: the FP8 forward quantizes V this way so that K6 can
+     carry V's per-block scale in the P codes exactly (an exponent shift). */
+  int32_t scale_pow2;
 } fa3b_fp8_prepare_params;
 
 typedef struct fa3b_bwd_params {

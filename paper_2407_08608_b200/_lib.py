@@ -80,6 +80,7 @@ class Fp8PrepareParams(ctypes.Structure):
         ("seed", ctypes.c_uint64),
         ("saturate", ctypes.c_int32),
         ("stream", ctypes.c_void_p),
+        ("scale_pow2", ctypes.c_int32),
     ]
 
 

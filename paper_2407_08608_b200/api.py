@@ -145,9 +145,12 @@ def fwd(q, k, v, *, causal: bool = False, alpha: float | None = None,
 
 
 def fp8_prepare(x, *, block_rows: int = 128, hadamard: bool = True, seed: int = 0,
-                saturate: bool = True, out=None, scales=None, stream=None):
+                saturate: bool = True, scale_pow2: bool = False, out=None, scales=None,
+                stream=None):
     """Random-sign Hadamard (optional) + per-block e4m3 quantization.
 
+    scale_pow2: power-of-two block scales (the smallest 2^e >= amax / 448) instead
+    of the reference's amax / 448; the FP8 forward quantizes V this way.
     Returns (codes [B, N, H, D] float8_e4m3fn, scales [B, H, nblocks] fp32)."""
     if x.dim() != 4 or x.numel() == 0:
         _fail(_lib.ERR_EMPTY, f"fp8_prepare input {tuple(x.shape)}")
@@ -171,6 +174,7 @@ def fp8_prepare(x, *, block_rows: int = 128, hadamard: bool = True, seed: int = 
     p.hadamard = int(bool(hadamard))
     p.seed = seed & 0xFFFFFFFFFFFFFFFF
     p.saturate = int(bool(saturate))
+    p.scale_pow2 = int(bool(scale_pow2))
     p.stream = _stream(stream)
     _lib.check(_lib.load().fa3b_fp8_prepare(ctypes.byref(p)))
     return out, scales
@@ -181,11 +185,14 @@ def fp8_fwd(q, k, v, *, causal: bool = False, alpha: float | None = None,
             schedule: str = "pingpong", out_dtype=None, stream=None):
     """The reference's fp8_flash_fwd (fp8_attention.cpp:77-181) on the device:
     K5 (Hadamard on Q and K with one seed, block or tensor quantization of Q,
-    K, V) then K6. Inputs are 16-bit or fp32 [B, N, H, D]; returns (O, LSE)."""
+    K, V) then K6. Inputs are 16-bit or fp32 [B, N, H, D]; returns (O, LSE).
+    Per block, V gets power-of-two scales (a documented deviation from the
+    reference's amax / 448: same e4m3 precision, and K6 applies each key block's
+    V scale exactly as an exponent shift of the P codes)."""
     blk = 128 if per_block else 0
     q8, sq = fp8_prepare(q, block_rows=blk, hadamard=incoherent, seed=seed, stream=stream)
     k8, sk = fp8_prepare(k, block_rows=blk, hadamard=incoherent, seed=seed, stream=stream)
-    v8, sv = fp8_prepare(v, block_rows=blk, hadamard=False, stream=stream)
+    v8, sv = fp8_prepare(v, block_rows=blk, hadamard=False, scale_pow2=per_block, stream=stream)
     return fwd(q8, k8, v8, causal=causal, alpha=alpha, schedule=schedule, out_dtype=out_dtype,
                q_scale=sq, k_scale=sk, v_scale=sv, q_block_rows=blk, kv_block_rows=blk,
                stream=stream)

@@ -24,6 +24,8 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstddef>
+#include <cstdlib>
 
 #include "../../include/fa3b.h"
 #include "fa3b_internal.cuh"
@@ -65,13 +67,24 @@ struct PrepArgs {
   uint8_t* dst;
   long long d_sb, d_ss, d_sh;
   float* scales;
-  int N, H, block_rows, nblk, hadamard, saturate;
+  int N, H, block_rows, nblk, hadamard, saturate, pow2;
   unsigned long long signs[4];  // bit i set -> sign_i = +1
 };
 
+// scale = amax / 448 (1 if amax == 0), quantize.cpp:41-42,54-55; with pow2 the
+// smallest power of two >= that value (fa3b_fp8_prepare_params.scale_pow2)
+__device__ __forceinline__ double block_scale(const PrepArgs& a, double amax) {
+  double scale = amax == 0.0 ? 1.0 : amax / 448.0;
+  if (a.pow2) {
+    const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(scale));
+    if (u & 0x000FFFFFFFFFFFFFull)
+      scale = __longlong_as_double(static_cast<long long>((u & 0x7FF0000000000000ull) + (1ull << 52)));
+  }
+  return scale;
+}
 __device__ __forceinline__ void write_scale(const PrepArgs& a, int b, int h, int blk, double amax,
                                             bool bad) {
-  const double scale = amax == 0.0 ? 1.0 : amax / 448.0;
+  const double scale = block_scale(a, amax);
   // non-finite inputs: the reference throws; the device reports a NaN scale
   a.scales[(static_cast<size_t>(b) * a.H + h) * a.nblk + blk] =
       bad ? __int_as_float(0x7fc00000) : static_cast<float>(scale);
@@ -280,7 +293,7 @@ __global__ void __launch_bounds__(512, 1) fa3b_fp8_prepare_quad_kernel(const Pre
       bad |= s_bad[sb][w] != 0;
     }
     if (threadIdx.x == 0) write_scale(a, b, h, blk, amax, bad);
-    const double inv = 1.0 / (amax == 0.0 ? 1.0 : amax / 448.0);  // quantize.cpp:25
+    const double inv = 1.0 / block_scale(a, amax);  // quantize.cpp:25
     if (row < a.N) quad_store<D>(a, b, h, row, qd, v, inv);
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -364,7 +377,7 @@ __global__ void __launch_bounds__(256) fa3b_fp8_prepare_kernel(const PrepArgs a)
     cluster_sync();  // keep every CTA's shared memory alive until all have read it
   }
   if (threadIdx.x == 0 && (C == 1 || cluster_rank() == 0)) write_scale(a, b, h, blk, amax, bad);
-  const double inv = 1.0 / (amax == 0.0 ? 1.0 : amax / 448.0);
+  const double inv = 1.0 / block_scale(a, amax);
   for (int it = 0; it < iters; ++it) {
     const int row = c0 + it * ROWS + rsub;
     double v[QD::Q];
@@ -406,6 +419,348 @@ cudaError_t launch_generic(const PrepArgs& a, dim3 grid, cudaStream_t st) {
   return launch_two_pass<D, 1>(a, grid, st);
 }
 
+// ---------------------------------------------------------------- fast path
+// bf16 input, 128-row blocks, saturating encode (the FP8 forward's case). The
+// same codes and scales as the FP64 kernels above, at a fraction of the work:
+//
+// * Transform in exact int32 arithmetic. A bf16 value is (128 + m) 2^(E - 134);
+//   scaled by 2^k (k = 157 - log2 d - E_max of the row) every entry of a row
+//   whose exponents span at most 23 - log2 d binades is an integer below
+//   2^(31 - log2 d), so FMUL by 2^k and F2I are exact and the int32 butterflies
+//   cannot overflow: the integer FWHT equals the reference's FP64 sums exactly
+//   (those sums are exact in FP64 too, so the order of additions is free).
+// * amax: max |S| per row is exact (ldexp of an integer), so amax =
+//   RN64(max|S| * norm) = max |RN64(S * norm)| is the reference's value bit for
+//   bit, and scale / inv follow with the reference's FP64 operations.
+// * Encode: t = RN64(RN64(S * norm) * inv) is approximated in FP32 by
+//   I2F(I) * RN32(2^-k * norm * inv) (relative error < 3.01 * 2^-24). The code is
+//   taken when the e4m3 conversions of t32 (1 -/+ 6 * 2^-24) agree (RNE is
+//   monotone, so every value in between, the exact t included, has that code);
+//   otherwise (~1e-5 of the entries) t is recomputed exactly in FP64.
+// * Rows outside the int32 range (exponent spread, zeros mixed with non-zeros,
+//   subnormals, non-finite values) are done by the whole warp in FP64 with the
+//   reference's operation order (fast_row_fp64), one row at a time.
+// Without the Hadamard (V) the FP32 encode of the exact bf16 value is used
+// directly. One CTA per 128-row block; lane group of LPR lanes per row, each
+// lane Q = 32 (d = 64: 16) contiguous elements.
+template <int D>
+struct Fast {
+  static constexpr int Q = D == 64 ? 16 : 32;
+  static constexpr int LPR = D / Q;           // 4, 4, 8
+  static constexpr int RPW = 32 / LPR;        // rows per warp
+  static constexpr int THREADS = 128 * LPR;   // 512, 512, 1024
+  static constexpr int WARPS = THREADS / 32;
+  static constexpr int LOGD = D == 64 ? 6 : (D == 128 ? 7 : 8);
+  static constexpr int SPREAD = 23 - LOGD;    // binades an int32 row may span
+};
+
+__device__ __forceinline__ uint32_t vmax_u16x2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("max.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t vmin_u16x2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("min.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ double pow2d(int e) {  // 2^e, |e| <= 1022
+  return __longlong_as_double(static_cast<long long>(1023 + e) << 52);
+}
+// saturating RNE e4m3 code of an FP64 value: FP64 -> FP32 round-to-odd, then the
+// hardware RNE (24 >= 4 + 2 bits, so the double rounding is exact)
+__device__ __forceinline__ uint32_t e4m3_sat(double t) {
+  float z = __double2float_rz(t);
+  if (static_cast<double>(z) != t) z = __uint_as_float(__float_as_uint(z) | 1u);
+  return ptx::pack_e4m3x4(z, 0.f, 0.f, 0.f) & 0xFFu;
+}
+
+// One row by the whole warp in FP64 (lane l holds entries [l M, l M + M)), the
+// reference's FWHT order: len = 1, 2, ... with (a + b, a - b) (hadamard.cpp:11-33).
+template <int D, bool HAD>
+__device__ __forceinline__ void fast_row_fp64(const PrepArgs& a, int b, int h, int row, int lane,
+                                              double (&s)[D / 32]) {
+  constexpr int M = D / 32;
+  const uint16_t* src = static_cast<const uint16_t*>(a.src) + b * a.s_sb +
+                        static_cast<size_t>(row) * a.s_ss + h * a.s_sh + lane * M;
+  uint16_t v16[M];
+  if constexpr (M == 2) {
+    const uint32_t u = *reinterpret_cast<const uint32_t*>(src);
+    v16[0] = u & 0xFFFF; v16[1] = u >> 16;
+  } else if constexpr (M == 4) {
+    const uint2 u = *reinterpret_cast<const uint2*>(src);
+    v16[0] = u.x & 0xFFFF; v16[1] = u.x >> 16; v16[2] = u.y & 0xFFFF; v16[3] = u.y >> 16;
+  } else {
+    const uint4 u = *reinterpret_cast<const uint4*>(src);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { v16[2 * i] = w[i] & 0xFFFF; v16[2 * i + 1] = w[i] >> 16; }
+  }
+#pragma unroll
+  for (int e = 0; e < M; ++e) s[e] = __uint_as_float(static_cast<uint32_t>(v16[e]) << 16);
+  if constexpr (HAD) {
+#pragma unroll
+    for (int e = 0; e < M; ++e) {
+      const int i = lane * M + e;
+      if (!((a.signs[i >> 6] >> (i & 63)) & 1ull)) s[e] = -s[e];
+    }
+#pragma unroll
+    for (int len = 1; len < M; len <<= 1)
+#pragma unroll
+      for (int e = 0; e < M; ++e)
+        if ((e & len) == 0) {
+          const double p = s[e], q = s[e + len];
+          s[e] = p + q;
+          s[e + len] = p - q;
+        }
+#pragma unroll
+    for (int m = 1; m < 32; m <<= 1) {
+      const double sgn = (lane & m) ? -1.0 : 1.0;
+#pragma unroll
+      for (int e = 0; e < M; ++e) s[e] = fma(sgn, s[e], __shfl_xor_sync(0xffffffffu, s[e], m));
+    }
+  }
+}
+
+// One CTA per 128-row block (grid = blocks x heads x batch); two CTAs per SM at
+// d <= 128 overlap one block's loads with the other's arithmetic. (Measured and
+// not kept: a persistent variant streaming the next block through cp.async, and
+// an L2 prefetch of the next wave's rows; profiles/r02/r02i_prep.log, r02l_prep.log.)
+template <int D, bool HAD>
+__global__ void __launch_bounds__(Fast<D>::THREADS, Fast<D>::THREADS == 512 ? 2 : 1)
+    fa3b_fp8_prepare_fast_kernel(const PrepArgs a) {
+  using F = Fast<D>;
+  constexpr int Q = F::Q, LPR = F::LPR, NP = Q / 2;
+  // t32 = RN(I2F(I) * RN(c kLo|Hi)) brackets the exact RN64(RN64(S norm) inv):
+  // relative error of I2F(I) * c is < 3.01 u, the bracket adds 2 u of rounding
+  constexpr float kLo = 1.f - 8.f / 16777216.f, kHi = 1.f + 8.f / 16777216.f;
+  __shared__ __align__(16) uint32_t s_mask[LPR * NP];  // sign flips per bf16 pair
+  __shared__ double s_red[F::WARPS];
+  __shared__ int s_bad[F::WARPS];
+  __shared__ double s_bc[2];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, qd = lane % LPR;
+  const int blk = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int row = blk * 128 + warp * F::RPW + lane / LPR;
+  const bool valid = row < a.N;
+  const double norm = HAD ? 1.0 / sqrt(static_cast<double>(D)) : 1.0;
+  if constexpr (HAD) {
+    for (int i = tid; i < LPR * NP; i += F::THREADS) {
+      const int e0 = (i / NP) * Q + 2 * (i % NP), e1 = e0 + 1;
+      const bool f0 = !((a.signs[e0 >> 6] >> (e0 & 63)) & 1ull);
+      const bool f1 = !((a.signs[e1 >> 6] >> (e1 & 63)) & 1ull);
+      s_mask[i] = (f0 ? 0x8000u : 0u) | (f1 ? 0x80000000u : 0u);
+    }
+  }
+  uint32_t w[NP];
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(
+        static_cast<const uint16_t*>(a.src) + b * a.s_sb + static_cast<size_t>(valid ? row : 0) * a.s_ss +
+        h * a.s_sh + qd * Q);
+#pragma unroll
+    for (int k = 0; k < Q / 8; ++k) {
+      const uint4 v = valid ? __ldg(src + k) : make_uint4(0, 0, 0, 0);
+      w[4 * k] = v.x; w[4 * k + 1] = v.y; w[4 * k + 2] = v.z; w[4 * k + 3] = v.w;
+    }
+  }
+  if constexpr (HAD) __syncthreads();  // s_mask
+  if constexpr (HAD) {
+    const uint4* mk = reinterpret_cast<const uint4*>(s_mask + qd * NP);
+#pragma unroll
+    for (int k = 0; k < NP / 4; ++k) {
+      const uint4 m = mk[k];
+      w[4 * k] ^= m.x; w[4 * k + 1] ^= m.y; w[4 * k + 2] ^= m.z; w[4 * k + 3] ^= m.w;
+    }
+  }
+  // exponent range of the row (16-bit magnitudes compare like the values)
+  uint32_t mx = 0, mn = 0xFFFFFFFFu;
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    const uint32_t m = w[p] & 0x7FFF7FFFu;
+    mx = vmax_u16x2(mx, m);
+    mn = vmin_u16x2(mn, m);
+  }
+  uint32_t mx16 = max(mx & 0xFFFFu, mx >> 16), mn16 = min(mn & 0xFFFFu, mn >> 16);
+#pragma unroll
+  for (int o = 1; o < LPR; o <<= 1) {
+    mx16 = max(mx16, __shfl_xor_sync(0xffffffffu, mx16, o));
+    mn16 = min(mn16, __shfl_xor_sync(0xffffffffu, mn16, o));
+  }
+  const int emax = static_cast<int>(mx16 >> 7), emin = static_cast<int>(mn16 >> 7);
+  const bool allzero = mx16 == 0;
+  const int k = 157 - F::LOGD - emax;
+  const bool fast = HAD ? (allzero || (emax <= 254 && emin >= 1 && emin >= emax - F::SPREAD && k <= 127))
+                        : emax <= 254;
+  // ---- transform (fast rows; other rows compute garbage that is never used)
+  int I[HAD ? Q : 1];
+  double rowS = 0.0;  // max |S| of this row (exact)
+  if constexpr (HAD) {
+    const float fs = (fast && !allzero) ? __uint_as_float(static_cast<uint32_t>(k + 127) << 23) : 0.f;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const float2 x = __fmul2_rn(make_float2(__uint_as_float(w[p] << 16), __uint_as_float(w[p] & 0xFFFF0000u)),
+                                  make_float2(fs, fs));
+      I[2 * p] = __float2int_rn(x.x);
+      I[2 * p + 1] = __float2int_rn(x.y);
+    }
+#pragma unroll
+    for (int len = 1; len < Q; len <<= 1)
+#pragma unroll
+      for (int e = 0; e < Q; ++e)
+        if ((e & len) == 0) {
+          const int p = I[e], q = I[e + len];
+          I[e] = p + q;
+          I[e + len] = p - q;
+        }
+#pragma unroll
+    for (int m = 1; m < LPR; m <<= 1) {
+      // lower lane a + b, upper lane a - b = other - mine: one IMAD with sgn = +-1
+      // (written as PTX mad: the compiler would otherwise select between I and -I)
+      const int sgn = (qd & m) ? -1 : 1;
+#pragma unroll
+      for (int e = 0; e < Q; ++e) {
+        const int other = __shfl_xor_sync(0xffffffffu, I[e], m);
+        asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(I[e]) : "r"(I[e]), "r"(sgn), "r"(other));
+      }
+    }
+    int hi_i = I[0], lo_i = I[0];
+#pragma unroll
+    for (int e = 1; e + 1 < Q; e += 2) {
+      hi_i = max(hi_i, max(I[e], I[e + 1]));
+      lo_i = min(lo_i, min(I[e], I[e + 1]));
+    }
+    hi_i = max(hi_i, I[Q - 1]);
+    lo_i = min(lo_i, I[Q - 1]);
+    int rm = max(hi_i, -lo_i);  // |I| < 2^31: no overflow
+#pragma unroll
+    for (int o = 1; o < LPR; o <<= 1) rm = max(rm, __shfl_xor_sync(0xffffffffu, rm, o));
+    rowS = fast ? static_cast<double>(rm) * pow2d(-k) : 0.0;
+  } else {
+    rowS = static_cast<double>(__uint_as_float(mx16 << 16));  // exact max |x| (finite rows)
+  }
+  // ---- rows outside the fast range: the whole warp, one row at a time, in FP64
+  bool bad = false;
+  const uint32_t slow_rows = __ballot_sync(0xffffffffu, !fast && valid && qd == 0);
+  for (uint32_t sr = slow_rows; sr != 0; sr &= sr - 1) {
+    const int src_lane = __ffs(sr) - 1;
+    const int r = blk * 128 + warp * F::RPW + src_lane / LPR;
+    double s[D / 32];
+    fast_row_fp64<D, HAD>(a, b, h, r, lane, s);
+    double m = 0.0;
+    bool nf = false;
+#pragma unroll
+    for (int e = 0; e < D / 32; ++e) {
+      nf |= !isfinite(s[e]);
+      m = fmax(m, fabs(s[e]));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    nf = __any_sync(0xffffffffu, nf);
+    if (lane / LPR == src_lane / LPR) {
+      rowS = m;
+      bad |= nf;
+    }
+  }
+  // ---- block amax, scale = amax / 448, inv = 1 / scale (quantize.cpp:25,55)
+  double v = rowS;
+#pragma unroll
+  for (int o = LPR; o < 32; o <<= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  bad = __any_sync(0xffffffffu, bad);
+  if (lane == 0) {
+    s_red[warp] = v;
+    s_bad[warp] = bad;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double m = s_red[0];
+    int bd = s_bad[0];
+#pragma unroll
+    for (int i = 1; i < F::WARPS; ++i) {
+      m = fmax(m, s_red[i]);
+      bd |= s_bad[i];
+    }
+    const double amax = m * norm;
+    write_scale(a, b, h, blk, amax, bd != 0);
+    const double inv = 1.0 / block_scale(a, amax);
+    s_bc[0] = inv;
+    s_bc[1] = norm * inv;
+  }
+  __syncthreads();
+  const double inv = s_bc[0];
+  // ---- encode
+  uint8_t* dst_row = a.dst + b * a.d_sb + static_cast<size_t>(row) * a.d_ss + h * a.d_sh;
+  if (fast && valid) {
+    float c;
+    if constexpr (HAD)
+      c = allzero ? 0.f : static_cast<float>(s_bc[1] * pow2d(-k));
+    else
+      c = inv < 1e38 ? static_cast<float>(inv) : 0.f;
+    const bool huge = !HAD && !(inv < 1e38);  // c would overflow FP32: encode exactly
+    // t32 * (1 -/+ 8 u) in one FMUL2 per entry: (x, x) * (c kLo, c kHi)
+    const float2 cc = make_float2(c * kLo, c * kHi);
+    uint32_t packed[Q / 4];
+    uint32_t miss = 0;  // groups of 4 whose bracket straddles an e4m3 rounding boundary
+#pragma unroll
+    for (int g = 0; g < Q / 4; ++g) {
+      float2 t[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float x;
+        if constexpr (HAD) {
+          x = static_cast<float>(I[4 * g + i]);
+        } else {
+          const uint32_t wp = w[2 * g + (i >> 1)];
+          x = __uint_as_float((i & 1) ? (wp & 0xFFFF0000u) : (wp << 16));
+        }
+        t[i] = __fmul2_rn(cc, make_float2(x, x));
+      }
+      const uint32_t lo = ptx::pack_e4m3x4(t[0].x, t[1].x, t[2].x, t[3].x);
+      const uint32_t hi = ptx::pack_e4m3x4(t[0].y, t[1].y, t[2].y, t[3].y);
+      packed[g] = lo;
+      miss |= static_cast<uint32_t>(lo != hi) << g;
+    }
+    if (huge) miss = ~0u;
+    if (miss != 0) {  // ~1e-5 of the entries: the exact FP64 encode for those groups
+#pragma unroll
+      for (int g = 0; g < Q / 4; ++g) {
+        if (!((miss >> g) & 1u)) continue;
+        uint32_t code = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          double td;
+          if constexpr (HAD) {
+            td = (static_cast<double>(I[4 * g + i]) * pow2d(-k) * norm) * inv;
+          } else {
+            const uint32_t wp = w[2 * g + (i >> 1)];
+            td = static_cast<double>(__uint_as_float((i & 1) ? (wp & 0xFFFF0000u) : (wp << 16))) * inv;
+          }
+          code |= e4m3_sat(td) << (8 * i);
+        }
+        packed[g] = code;
+      }
+    }
+    uint4* dst = reinterpret_cast<uint4*>(dst_row + qd * Q);
+#pragma unroll
+    for (int k2 = 0; k2 < Q / 16; ++k2)
+      dst[k2] = make_uint4(packed[4 * k2], packed[4 * k2 + 1], packed[4 * k2 + 2], packed[4 * k2 + 3]);
+  }
+  for (uint32_t sr = slow_rows; sr != 0; sr &= sr - 1) {
+    const int src_lane = __ffs(sr) - 1;
+    const int r = blk * 128 + warp * F::RPW + src_lane / LPR;
+    double s[D / 32];
+    fast_row_fp64<D, HAD>(a, b, h, r, lane, s);
+    uint32_t cw[(D / 32 + 3) / 4] = {};
+#pragma unroll
+    for (int e = 0; e < D / 32; ++e) cw[e >> 2] |= e4m3_sat((s[e] * norm) * inv) << (8 * (e & 3));
+    uint8_t* drow = a.dst + b * a.d_sb + static_cast<size_t>(r) * a.d_ss + h * a.d_sh + lane * (D / 32);
+    if constexpr (D / 32 == 2)
+      *reinterpret_cast<uint16_t*>(drow) = static_cast<uint16_t>(cw[0]);
+    else if constexpr (D / 32 == 4)
+      *reinterpret_cast<uint32_t*>(drow) = cw[0];
+    else
+      *reinterpret_cast<uint2*>(drow) = make_uint2(cw[0], cw[1]);
+  }
+}
+
 uint64_t mix64(uint64_t z) {  // rng.cpp:15-19
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
@@ -420,7 +775,10 @@ using namespace fa3b;
 extern "C" int fa3b_fp8_prepare(const fa3b_fp8_prepare_params* pp) {
   g_last_launch_count = 0;
   if (pp == nullptr) return FA3B_ERR_NULL;
-  if (pp->struct_size != sizeof(fa3b_fp8_prepare_params)) return FA3B_ERR_STRUCT;
+  // ABI 1 callers pass the struct without scale_pow2
+  if (pp->struct_size != sizeof(fa3b_fp8_prepare_params) &&
+      pp->struct_size != offsetof(fa3b_fp8_prepare_params, scale_pow2))
+    return FA3B_ERR_STRUCT;
   const auto& p = *pp;
   if (p.batch <= 0 || p.heads <= 0 || p.seqlen <= 0 || p.head_dim <= 0) return FA3B_ERR_EMPTY;
   if (p.hadamard && (p.head_dim & (p.head_dim - 1))) return FA3B_ERR_NOT_POW2;
@@ -449,6 +807,7 @@ extern "C" int fa3b_fp8_prepare(const fa3b_fp8_prepare_params* pp) {
   a.nblk = p.block_rows ? (p.seqlen + p.block_rows - 1) / p.block_rows : 1;
   a.hadamard = p.hadamard;
   a.saturate = p.saturate;
+  a.pow2 = p.struct_size == sizeof(fa3b_fp8_prepare_params) && p.scale_pow2 != 0;
   // sample_sign_vector(d, seed): sign_i = +1 iff word(i) = mix64(seed + (i+1) gamma) is odd
   for (int i = 0; i < p.head_dim; ++i)
     if (mix64(p.seed + static_cast<uint64_t>(i + 1) * 0x9E3779B97F4A7C15ull) & 1ull)
@@ -456,7 +815,31 @@ extern "C" int fa3b_fp8_prepare(const fa3b_fp8_prepare_params* pp) {
   dim3 grid(a.nblk, p.heads, p.batch);
   cudaStream_t st = static_cast<cudaStream_t>(p.stream);
   cudaError_t e = cudaSuccess;
-  if (p.block_rows == 128 && p.head_dim <= 128) {
+  static const bool fast_env = [] {
+    const char* e = std::getenv("FA3B_K5_FAST");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  if (fast_env && p.block_rows == 128 && p.src_dtype == FA3B_DTYPE_BF16 && p.saturate) {
+    auto go = [&](auto kern, int threads) {
+      kern<<<grid, threads, 0, st>>>(a);
+      return cudaGetLastError();
+    };
+    switch (p.head_dim) {
+      case 64:
+        e = p.hadamard ? go(fa3b_fp8_prepare_fast_kernel<64, true>, Fast<64>::THREADS)
+                       : go(fa3b_fp8_prepare_fast_kernel<64, false>, Fast<64>::THREADS);
+        break;
+      case 128:
+        e = p.hadamard ? go(fa3b_fp8_prepare_fast_kernel<128, true>, Fast<128>::THREADS)
+                       : go(fa3b_fp8_prepare_fast_kernel<128, false>, Fast<128>::THREADS);
+        break;
+      default:
+        e = p.hadamard ? go(fa3b_fp8_prepare_fast_kernel<256, true>, Fast<256>::THREADS)
+                       : go(fa3b_fp8_prepare_fast_kernel<256, false>, Fast<256>::THREADS);
+        break;
+    }
+    if (e != cudaSuccess) return cuda_fail(e);
+  } else if (p.block_rows == 128 && p.head_dim <= 128) {
     // d = 256 would hold 64 doubles per thread; it takes the two-pass kernel instead
     const int items = a.nblk * p.heads * p.batch;
     // persistent at d = 128 (+7 %); d = 64 (half the FP64 work per block) was faster

@@ -33,15 +33,19 @@
 // KIND = E4M3 is the FP8 forward K6 (fp8_flash_fwd, core/src/fp8_attention.cpp:
 // 77-181): Q/K/V are e4m3 codes with per-128-row-block (or per-tensor) scales
 // from K5; the S descale alpha s_q s_k[j] folds into the exp2 pre-scale
-// (PAPER.md:605-606); P is requantized to e4m3 with the fixed scale 2^THR/448
-// (THR = args.fp8_thr) instead of the reference's per-block amax, which is
-// ~1 for every block (proj/README.md:116-121). V's per-block scale is applied
-// exactly, as the reference does to each PV product (fp8_attention.cpp:158-164):
-// O is kept in units of the current block's s_v, i.e. rescaled by
-// s_v[j-1] / s_v[j] in the same TMEM pass as the softmax rescale, and the last
-// s_v is applied in the epilogue. (Folding s_v into P instead costs ~15% RMSE
-// on outlier inputs because small P codes drop into e4m3 subnormals.) Both MMAs run as tcgen05 kind::f8f6f4 with V consumed
-// MN-major straight from the TMA tile (no in-kernel transpose on sm_100a).
+// (PAPER.md:605-606); P is requantized to e4m3 with the fixed scale 448 / 2^THR
+// (THR = args.fp8_thr, the lazy-max headroom) instead of the reference's
+// per-block amax, which is ~1 for every block (proj/README.md:116-121). V's
+// per-block scale is applied exactly, as the reference does to each PV product
+// (fp8_attention.cpp:158-164): O is kept in units of a V scale v_cur. When a key
+// block's s_v / v_cur is an exact power of two in [2^-8, 1] (the FP8 forward
+// quantizes V with power-of-two block scales, fa3b.h scale_pow2) the ratio is
+// folded into that block's P codes, an exact exponent shift; otherwise O is
+// rescaled to s_v (one TMEM pass, shared with the softmax rescale). Folding an
+// arbitrary ratio instead makes the codes of the largest P inexact and cost
+// +14 % RMSE on the reference's outlier inputs (profiles/r02/r02f_acc.log).
+// Both MMAs run as tcgen05 kind::f8f6f4 with V consumed MN-major straight from
+// the TMA tile (no in-kernel transpose on sm_100a).
 //
 // One query tile per CTA (d = 256 and the basic schedule; T::S2): TMEM has
 // room for a second S buffer after O, so the MMA warp computes S(K_{j+1}) while
@@ -133,9 +137,7 @@ struct FwdArgs {
   const float* v_scale;
   int q_blocked, kv_blocked;
   float fp8_thr;         // lazy-rescale threshold (log2) for the e4m3 P
-  float fp8_pmul, fp8_inv_pmul, fp8_lpm;  // P code scale, its inverse and log2 (host-computed):
-                                          // 448 / 2^thr, or 224 / 2^thr with per-block V
-                                          // scales (headroom for the folded V ratio)
+  float fp8_pmul, fp8_inv_pmul, fp8_lpm;  // P code scale 448 / 2^thr, its inverse and log2
 };
 __device__ __forceinline__ int fwd_seqlen(const FwdArgs& a) { return a.N; }
 
@@ -774,6 +776,23 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
     auto tmem_stw = [](uint32_t a, const uint32_t (&v)[CW]) {
       if constexpr (CW == 32) ptx::tmem_st32(a, v); else ptx::tmem_st16(a, v);
     };
+    auto rescale_o = [&](float f) {
+      constexpr int NC = DH / CW;
+      constexpr int G = NC < 4 ? NC : 4;
+#pragma unroll
+      for (int c0 = 0; c0 < NC; c0 += G) {
+        uint32_t ov[G][CW];
+#pragma unroll
+        for (int c = 0; c < G; ++c) tmem_ldw(tO + DH * hh + (c0 + c) * CW, ov[c]);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < G; ++c) {
+#pragma unroll
+          for (int i = 0; i < CW; ++i) ov[c][i] = __float_as_uint(__uint_as_float(ov[c][i]) * f);
+          tmem_stw(tO + DH * hh + (c0 + c) * CW, ov[c]);
+        }
+      }
+    };
     float sl2 = args.scale_log2;
     const float thr = FP8 ? args.fp8_thr : 8.f;
     float out_scale = 1.f;
@@ -795,10 +814,12 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
     const float lpm = FP8 ? args.fp8_lpm : 0.f;
     // per-block K / V scales of the next block are fetched one iteration ahead
     float ks_next = 1.f, vs_next = 1.f;
+    const float* ksp = FP8 ? args.k_scale + ks_base : nullptr;
+    const float* vsp = FP8 ? args.v_scale + ks_base : nullptr;
     if constexpr (FP8) {
       if (nt > 0) {
-        ks_next = args.k_scale[ks_base];
-        vs_next = args.v_scale[ks_base];
+        ks_next = ksp[0];
+        vs_next = vsp[0];
       }
     }
     for (int j = 0; j < nt; ++j) {
@@ -809,19 +830,24 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
         slj = sl2 * ks_next;
         const float vs = vs_next;
         if (args.kv_blocked && j + 1 < nt) {
-          ks_next = args.k_scale[ks_base + j + 1];
-          vs_next = args.v_scale[ks_base + j + 1];
+          ks_next = ksp[j + 1];
+          vs_next = vsp[j + 1];
         }
         if (vs != v_cur) {
-          // O stays in units of v_cur while rho = s_v[j] / v_cur is in [1/2, 2): the
-          // ratio scales this block's P codes instead (the P scale keeps one bit of
-          // headroom for it), so O is rescaled only when rho leaves that range
-          const float rho = vs / v_cur;  // inf on the first block (v_cur = 0)
-          if (rho >= 0.5f && rho < 2.f) {
-            lrho = __log2f(rho);
-            inv_rho = v_cur / vs;
+          // O stays in units of v_cur while rho = s_v[j] / v_cur is an exact power of
+          // two in [2^-8, 1] (equal mantissas): rho then scales this block's P codes
+          // exactly (an exponent shift), so O is rescaled only at a new maximum of the
+          // V scales. Per-block V scales that are powers of two (fa3b_fp8_prepare with
+          // scale_pow2, as the FP8 forward quantizes V) fold at every other block; any
+          // other ratio rescales O to s_v[j], the reference's exact per-block
+          // s_v (fp8_attention.cpp:158-164).
+          const uint32_t ub = __float_as_uint(vs), uc = __float_as_uint(v_cur);
+          const int de = static_cast<int>(ub >> 23) - static_cast<int>(uc >> 23);
+          if (((ub ^ uc) & 0x807FFFFFu) == 0 && de <= 0 && de >= -8 && v_cur != 0.f) {
+            lrho = static_cast<float>(de);
+            inv_rho = __uint_as_float(static_cast<uint32_t>(127 - de) << 23);
           } else {
-            vfac = v_cur / vs;  // 0 on the first block: O is empty
+            vfac = v_cur == 0.f ? 0.f : __fdividef(v_cur, vs);  // 0 on the first block: O is empty
             v_cur = vs;
           }
         }
@@ -897,7 +923,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
           const float2 x = __ffma2_rn(make_float2(s[2 * i], s[2 * i + 1]), sc2, nm2);
           float2 pp;
           if ((i & 7) < EMU) {
-            pp = ptx::ex2_poly2(x);
+            pp = FP8 ? ptx::ex2_poly2_d2(x) : ptx::ex2_poly2(x);
           } else {
             pp.x = ptx::ex2(x.x);
             pp.y = ptx::ex2(x.y);
@@ -941,25 +967,8 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       // wait only when O needs rescaling hung at bf16 d = 256)
       if constexpr ((T::S2 || T::S3) && !T::TWO_STAGE)
         if (j > 0) ptx::mbar_wait(&pv_done[t], (sc - 2) & 1);
-      if (j > 0 && __any_sync(0xffffffffu, ofac != 1.f)) {
-        // PV(V_{j-1}) is complete (see header / above); rescale this thread's O_t columns.
-        constexpr int NC = DH / CW;
-        constexpr int G = NC < 4 ? NC : 4;
-#pragma unroll
-        for (int c0 = 0; c0 < NC; c0 += G) {
-          uint32_t ov[G][CW];
-#pragma unroll
-          for (int c = 0; c < G; ++c) tmem_ldw(tO + DH * hh + (c0 + c) * CW, ov[c]);
-          ptx::tmem_wait_ld();
-#pragma unroll
-          for (int c = 0; c < G; ++c) {
-#pragma unroll
-            for (int i = 0; i < CW; ++i)
-              ov[c][i] = __float_as_uint(__uint_as_float(ov[c][i]) * ofac);
-            tmem_stw(tO + DH * hh + (c0 + c) * CW, ov[c]);
-          }
-        }
-      }
+      // PV(V_{j-1}) is complete (see header / above); rescale this thread's O_t columns.
+      if (j > 0 && __any_sync(0xffffffffu, ofac != 1.f)) rescale_o(ofac);
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
       __syncwarp();

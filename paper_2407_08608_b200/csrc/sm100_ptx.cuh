@@ -86,6 +86,24 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// try_wait with a suspend-time hint: the warp sleeps until the phase completes
+// (or ~1 ms passes) instead of spinning, so waiting warps take no issue slots
+// from the warps sharing their scheduler.
+#ifndef FA3B_WAIT_SLEEP
+#define FA3B_WAIT_SLEEP 1
+#endif
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint32_t bar, uint32_t parity) {
+  if (!FA3B_WAIT_SLEEP) return mbar_try_wait(bar, parity);
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity), "r"(1000000u)
+      : "memory");
+  return ok != 0;
+}
 // Blocks until the phase with the given parity has completed. With the
 // watchdog on, a wait that exceeds ~2^34 cycles (several seconds) traps so a
 // protocol bug surfaces as a launch error instead of a hung device.
@@ -93,8 +111,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   if (mbar_try_wait(a, parity)) return;
 #if FA3B_WATCHDOG
+  if (mbar_try_wait_sleep(a, parity)) return;
   const long long t0 = clock64();
-  while (!mbar_try_wait(a, parity)) {
+  while (!mbar_try_wait_sleep(a, parity)) {
     if (clock64() - t0 > (1ll << FA3B_WATCHDOG_LOG2)) {
 #ifdef FA3B_WATCHDOG_PRINT
       printf("fa3b watchdog: block %d thread %d smem bar 0x%x parity %u\n", blockIdx.x, threadIdx.x, a, parity);
@@ -103,7 +122,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
   }
 #else
-  while (!mbar_try_wait(a, parity)) {
+  while (!mbar_try_wait_sleep(a, parity)) {
   }
 #endif
 }
@@ -421,6 +440,20 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   float2 p = __ffma2_rn(f, make_float2(0.05500893294811249f, 0.05500893294811249f),
                         make_float2(0.24221095442771912f, 0.24221095442771912f));
   p = __ffma2_rn(p, f, make_float2(0.6932829022407532f, 0.6932829022407532f));
+  p = __ffma2_rn(p, f, make_float2(1.f, 1.f));
+  return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
+                     __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
+}
+// Degree-2 variant (p(0) = 1 exactly, max relative error 2.0e-3): enough for
+// e4m3 P codes, whose quantum is 2^-3 relative.
+__device__ __forceinline__ float2 ex2_poly2_d2(float2 x) {
+  constexpr float kMagic = 12582912.f;  // 1.5 * 2^23
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
+  const float2 t = __fadd2_rn(x, make_float2(kMagic, kMagic));
+  const float2 r = __fadd2_rn(t, make_float2(-kMagic, -kMagic));
+  const float2 f = __ffma2_rn(r, make_float2(-1.f, -1.f), x);
+  float2 p = __ffma2_rn(f, make_float2(0.23986253f, 0.23986253f), make_float2(0.70294039f, 0.70294039f));
   p = __ffma2_rn(p, f, make_float2(1.f, 1.f));
   return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
                      __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));

@@ -70,7 +70,7 @@ def test_flop_counts_and_version(fa3b_lib):
     assert fa3b_lib.fa3b_flops_forward(512, 64, 32, 1) == 1073741824
     assert fa3b_lib.fa3b_flops_backward(512, 64, 32, 0) == 2147483648 * 5 // 2
     assert fa3b_lib.fa3b_flops_forward(1, 1, 1, 0) == 4
-    assert fa3b_lib.fa3b_abi_version() == 1
+    assert fa3b_lib.fa3b_abi_version() == 2
 
 
 def _fwd_params(**kw):

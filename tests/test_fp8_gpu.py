@@ -184,3 +184,116 @@ def test_fp8_one_tile_many_items(cuda, B, N, H, D, causal, per_block):
             err, err_emu = (o[b, rows, h] - ref).norm().item(), (emu - ref).norm().item()
             assert err <= 1.3 * err_emu + 1e-3 * ref.norm().item(), (err, err_emu)
             assert (lse[b, h, rows] - torch.logsumexp(s, -1)).abs().max().item() < 0.05
+
+
+def _bf16_rows(kind, N, D, rng):
+    """float32 matrices of bf16-exact values exercising the fast K5 path's cases:
+    int32-exact rows, rows outside the int32 range (exponent spread, zeros mixed
+    with non-zeros, subnormals), all-zero rows and blocks, extreme magnitudes."""
+    import torch
+    x = rng.standard_normal((N, D)).astype(np.float32) * 3
+    if kind == "wide":  # every 7th row spans > 23 - log2(d) binades -> FP64 rows
+        x[::7, 0] *= 2.0 ** 20
+        x[3::11, 1] *= 2.0 ** -30
+    elif kind == "zeros":
+        x[::5, ::9] = 0.0          # zeros next to non-zeros
+        x[1::13] = 0.0             # all-zero rows
+        x[256:384] = 0.0           # an all-zero 128-row block
+    elif kind == "tiny":
+        x *= np.float32(2.0 ** -120)   # int path at the small end (k near 127)
+        x[::6] *= np.float32(2.0 ** -12)  # subnormal bf16 values
+    elif kind == "huge":
+        x *= np.float32(2.0 ** 100)
+    return torch.from_numpy(x).bfloat16().float().numpy()
+
+
+@pytest.mark.parametrize("D", [64, 128, 256])
+@pytest.mark.parametrize("hadamard", [True, False])
+@pytest.mark.parametrize("kind", ["gauss", "wide", "zeros", "tiny", "huge"])
+def test_prepare_bf16_fast_path_byte_exact(port, cuda, D, hadamard, kind):
+    # the bf16 / 128-row-block kernel (int32 transform, FP32 encode with an exact
+    # FP64 fallback) against the oracle's FP64 preprocess_incoherent + quantize
+    from paper_2407_08608_b200 import api
+    import torch
+    rng = np.random.default_rng(D * 7 + hadamard + len(kind))
+    B, N, H = 1, 1000, 2
+    x = np.stack([_bf16_rows(kind, N, D, rng) for _ in range(H)], axis=1)[None]  # [1, N, H, D]
+    xd = torch.from_numpy(x).cuda().bfloat16()
+    codes, scales = api.fp8_prepare(xd, block_rows=128, hadamard=hadamard, seed=4321)
+    codes = codes.float().cpu().numpy()
+    scales = scales.cpu().numpy()
+    for h in range(H):
+        m = x[0, :, h].astype(np.float64)
+        if hadamard:
+            m, _ = port.preprocess_incoherent(m, m, 4321)
+        want_c, want_s = port.quantize(m, 128)
+        assert np.array_equal(scales[0, h], want_s.astype(np.float32)), h
+        bad = np.argwhere(codes[0, :, h] != want_c)
+        assert bad.size == 0, (h, bad[:5])
+
+
+def test_prepare_bf16_fast_path_full_size(port, cuda):
+    # C2 shape of one (batch, head) pair at N 8192, d 128: byte-exact at full size
+    from paper_2407_08608_b200 import api
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn(1, 8192, 2, 128, device="cuda", generator=g, dtype=torch.bfloat16)
+    for had in (True, False):
+        codes, scales = api.fp8_prepare(x, block_rows=128, hadamard=had, seed=77)
+        for h in range(2):
+            m = x[0, :, h].double().cpu().numpy()
+            if had:
+                m, _ = port.preprocess_incoherent(m, m, 77)
+            want_c, want_s = port.quantize(m, 128)
+            assert np.array_equal(codes[0, :, h].float().cpu().numpy(), want_c), (had, h)
+            assert np.array_equal(scales[0, h].cpu().numpy(), want_s.astype(np.float32)), (had, h)
+
+
+def test_prepare_bf16_nonfinite_block_reports_nan_scale(cuda):
+    # the reference throws on non-finite input (quantize.cpp:15); the device marks
+    # the block's scale NaN and leaves the other blocks intact
+    from paper_2407_08608_b200 import api
+    import torch
+    x = torch.randn(1, 384, 1, 128, device="cuda", dtype=torch.bfloat16)
+    x[0, 200, 0, 5] = float("inf")
+    _, s = api.fp8_prepare(x, block_rows=128, hadamard=True, seed=3)
+    s = s.cpu()
+    assert torch.isnan(s[0, 0, 1]) and torch.isfinite(s[0, 0, 0]) and torch.isfinite(s[0, 0, 2])
+
+
+def _quantize_pow2(port, m, block_rows=128):
+    """quantize_per_block (quantize.cpp:47-60) with the scale raised to the
+    smallest power of two >= amax / 448 (fa3b_fp8_prepare_params.scale_pow2)."""
+    codes, scales = np.empty_like(m), []
+    for r0 in range(0, m.shape[0], block_rows):
+        blk = m[r0:r0 + block_rows]
+        amax = float(np.abs(blk).max())
+        s = amax / 448.0 if amax != 0.0 else 1.0
+        mant, ex = np.frexp(s)
+        if mant != 0.5:
+            s = 2.0 ** ex
+        codes[r0:r0 + block_rows] = port.round_array(blk * (1.0 / s), O.E4M3)
+        scales.append(s)
+    return codes, np.array(scales)
+
+
+@pytest.mark.parametrize("D", [64, 128, 256])
+@pytest.mark.parametrize("src", ["bf16", "f32"])
+@pytest.mark.parametrize("hadamard", [True, False])
+def test_prepare_pow2_scales_byte_exact(port, cuda, D, src, hadamard):
+    from paper_2407_08608_b200 import api
+    import torch
+    rng = np.random.default_rng(D + hadamard)
+    x = np.stack([_bf16_rows("gauss", 700, D, rng) for _ in range(2)], axis=1)[None]
+    xd = torch.from_numpy(x).cuda()
+    xd = xd.bfloat16() if src == "bf16" else xd.float()
+    codes, scales = api.fp8_prepare(xd, block_rows=128, hadamard=hadamard, seed=99, scale_pow2=True)
+    codes, scales = codes.float().cpu().numpy(), scales.cpu().numpy()
+    for h in range(2):
+        m = x[0, :, h].astype(np.float64)
+        if hadamard:
+            m, _ = port.preprocess_incoherent(m, m, 99)
+        want_c, want_s = _quantize_pow2(port, m)
+        assert np.array_equal(scales[0, h], want_s.astype(np.float32)), h
+        assert np.array_equal(codes[0, :, h], want_c), h
+        assert np.all(np.log2(scales[0, h]) == np.round(np.log2(scales[0, h])))

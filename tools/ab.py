@@ -28,8 +28,8 @@ for D, causal in ((128, False), (128, True), (64, False), (256, False)):
     cases.append((f"bf16 d{D}{'c' if causal else ''}", fl, (lambda q=q, k=k, v=v, c=causal: api.fwd(q, k, v, causal=c))))
     if D >= 128 and not causal:
         for blk, nm in ((128, "fp8"), (0, "fp8pt")):
-            _lib._lib = libs[0]
-            p = [api.fp8_prepare(x, block_rows=blk, hadamard=i < 2, seed=1) for i, x in enumerate((q, k, v))]
+            _lib._lib = libs[-1]
+            p = [api.fp8_prepare(x, block_rows=blk, hadamard=i < 2, seed=1, scale_pow2=(i == 2 and blk > 0)) for i, x in enumerate((q, k, v))]
             cases.append((f"{nm} d{D}", fl, (lambda p=p, blk=blk: api.fwd(p[0][0], p[1][0], p[2][0], q_scale=p[0][1], k_scale=p[1][1], v_scale=p[2][1], q_block_rows=blk, kv_block_rows=blk))))
 res = {(c[0], i): [] for c in cases for i in range(len(libs))}
 for name, fl, f in cases:

@@ -9,7 +9,7 @@ D, C, F = $D, bool($C), bool($F)
 N, B, H = 8192, 2, 2048 // D
 q, k, v = (torch.randn(B, N, H, D, device="cuda", dtype=torch.bfloat16) for _ in range(3))
 if F:
-    p = [api.fp8_prepare(x, block_rows=128, hadamard=i < 2, seed=1) for i, x in enumerate((q, k, v))]
+    p = [api.fp8_prepare(x, block_rows=128, hadamard=i < 2, seed=1, scale_pow2=i == 2) for i, x in enumerate((q, k, v))]
     f = lambda: api.fwd(p[0][0], p[1][0], p[2][0], causal=C, q_scale=p[0][1], k_scale=p[1][1], v_scale=p[2][1])
 else:
     f = lambda: api.fwd(q, k, v, causal=C)

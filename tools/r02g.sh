@@ -1,0 +1,9 @@
+set -u
+mkdir -p gpurun_out
+T=r02g
+timeout 900 python -m pytest tests/test_fp8_gpu.py -x -q > gpurun_out/${T}_pytest_fp8.log 2>&1; echo "pytest fp8 rc=$?"
+FA3B_K5_FAST=0 timeout 300 python tools/prep_time.py > gpurun_out/${T}_prep.log 2>&1
+FA3B_K5_FAST=1 timeout 300 python tools/prep_time.py >> gpurun_out/${T}_prep.log 2>&1; echo "prep rc=$?"
+timeout 300 python tools/fp8_acc.py > gpurun_out/${T}_acc.log 2>&1; echo "acc rc=$?"
+timeout 600 python tools/ab.py build/variants/base.so paper_2407_08608_b200/libfa3b.so > gpurun_out/${T}_ab.log 2>&1; echo "ab rc=$?"
+timeout 600 python -m pytest tests/test_report.py tests/test_fwd_gpu.py -x -q > gpurun_out/${T}_pytest_rest.log 2>&1; echo "pytest rest rc=$?"

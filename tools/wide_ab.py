@@ -34,7 +34,7 @@ for d, n, causal, dt in pts:
     g = torch.Generator(device="cuda").manual_seed(n + d)
     q, k, v = (torch.randn(B, n, H, d, device="cuda", generator=g).bfloat16() for _ in range(3))
     if dt == "e4m3":
-        pr = [api.fp8_prepare(x, block_rows=128, hadamard=i < 2, seed=1) for i, x in enumerate((q, k, v))]
+        pr = [api.fp8_prepare(x, block_rows=128, hadamard=i < 2, seed=1, scale_pow2=i == 2) for i, x in enumerate((q, k, v))]
         fn = lambda: api.fwd(pr[0][0], pr[1][0], pr[2][0], causal=causal, q_scale=pr[0][1],  # noqa: E731
                              k_scale=pr[1][1], v_scale=pr[2][1])
     else:
