@@ -315,7 +315,7 @@ def sweep(api, torch, dev, stream, fp8_peak):
                     fn=lambda: api.fwd(q, k, v, causal=causal, out=o, lse=lse, stream=stream))
             del q, k, v, o, lse
     # C3: FP8 forward
-    for d in (128, 256):
+    for d in (128, 64, 256):
         for n in seqlens:
             B, H = 16384 // n, 2048 // d
             x = [torch.randn(B, n, H, d, device=dev, dtype=torch.bfloat16) for _ in range(3)]
@@ -566,7 +566,9 @@ def run_ours(args, rank, world, local_rank):
         "dtype": "e4m3" if fp8 else "bf16",
         "data": "synthetic (torch.randn bf16 Q/K/V on device"
                 + ("; e4m3 codes + per-block scales from K5)" if fp8 else ")"),
-        "config": {"workload": w["name"], "global_batch": B_all, "seq_len": N,
+        "config": {"workload": (w["name"].replace("bf16", "e4m3") if "bf16" in w["name"]
+                                else w["name"] + " e4m3") if fp8 else w["name"],
+                   "global_batch": B_all, "seq_len": N,
                    "heads": H, "heads_kv": Hkv, "head_dim": D, "causal": causal,
                    "parallelism": (f"batch-sharded x{world} (no collectives)" if weak else
                                    f"KV-head-sharded x{world}, strided views (no collectives)"),

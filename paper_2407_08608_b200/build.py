@@ -29,7 +29,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CUDA_SOURCES = ["fa3b_capi.cu", "fwd16_d64.cu", "fwd16_d128.cu", "fwd16_d256.cu",
                 "fwd16_sched_bf16_c0.cu", "fwd16_sched_bf16_c1.cu", "fwd16_sched_f16_c0.cu",
-                "fwd16_sched_f16_c1.cu", "fwd_fp8.cu", "fp8_prepare.cu", "bwd.cu"]
+                "fwd16_sched_f16_c1.cu", "fwd_fp8.cu", "fwd_fp8_d64.cu", "fp8_prepare.cu", "bwd.cu"]
 COMPAT_SOURCES = ["flashlab_compat.cpp"]
 
 

@@ -586,7 +586,14 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
       uint32_t sr[64];
       ptx::tmem_ld32(tmem + lane_base + T::COL_S + 64 * w, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
       ptx::tmem_ld32(tmem + lane_base + T::COL_S + 64 * w + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
-      if (T::VEC_OWN) ptx::mbar_wait(&vec_full[s], (gi >> 1) & 1);
+      // LSE2_i / D_i arrived by cp.async.bulk on their own barrier (d = 128) or on
+      // Q_i's ring barrier (d = 64): wait on it here so the async-proxy writes are
+      // acquired by these threads directly (not only through the MMA warp's
+      // s_full commit; compute-sanitizer racecheck flagged that chain at d = 64)
+      if (T::VEC_OWN)
+        ptx::mbar_wait(&vec_full[s], (gi >> 1) & 1);
+      else
+        ptx::mbar_wait(&ring_full[slot_of(2 * gi)], par_of(2 * gi));
       ptx::tmem_wait_ld();
       const bool diag = CAUSAL && i == j;
       const int lim = kv_row - (i * 128 + 64 * w);  // causal: query column c is visible iff c >= lim

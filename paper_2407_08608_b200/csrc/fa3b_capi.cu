@@ -113,7 +113,7 @@ int ensure_smem_attr(const void* kernel, int bytes) {
 // [batch, seq, head, dim] tensor -> 4D map (dim, head, seq, batch) with a box
 // of (inner_elems, 1, rows, 1) and 128B swizzle. OOB rows read as zero.
 int make_tmap_4d(CUtensorMap* map, const fa3b_tensor4& t, int elem_bytes, int dim, int heads,
-                 int seqlen, int batch, int inner_elems, int rows) {
+                 int seqlen, int batch, int inner_elems, int rows, int swizzle_bytes) {
   EncodeTiledFn fn = encode_fn();
   if (fn == nullptr) return cuda_fail(cudaErrorNotSupported);
   CUtensorMapDataType dt = elem_bytes == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
@@ -128,7 +128,8 @@ int make_tmap_4d(CUtensorMap* map, const fa3b_tensor4& t, int elem_bytes, int di
                        1u};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = fn(map, dt, 4, t.ptr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return cuda_fail(cudaErrorInvalidValue);
   return FA3B_OK;

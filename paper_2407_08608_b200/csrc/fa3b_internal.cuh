@@ -12,14 +12,16 @@ extern thread_local int g_last_cuda_error;
 extern thread_local int g_last_launch_count;
 
 int cuda_fail(cudaError_t e);
+// swizzle_bytes: 128 (the default) or 64 (64-byte rows, e4m3 at d = 64)
 int make_tmap_4d(CUtensorMap* map, const fa3b_tensor4& t, int elem_bytes, int dim, int heads,
-                 int seqlen, int batch, int inner_elems, int rows);
+                 int seqlen, int batch, int inner_elems, int rows, int swizzle_bytes = 128);
 bool aligned16(const void* p);
 bool strides_ok(const fa3b_tensor4& t, int elem_bytes, int batch, int seqlen, int heads);
 int validate_problem(int batch, int heads_q, int heads_kv, int seqlen, int head_dim,
                      double alpha);
 
 int launch_fwd_fp8(const fa3b_fwd_params& p, cudaStream_t stream);
+int launch_fwd_fp8_d64(const fa3b_fwd_params& p, cudaStream_t stream);
 // f16/bf16 forward launchers, one translation unit each (fwd16_*.cu)
 int launch_fwd16_default_d64(const fa3b_fwd_params& p, cudaStream_t s, bool cta_pairs);
 int launch_fwd16_default_d128(const fa3b_fwd_params& p, cudaStream_t s, bool cta_pairs);

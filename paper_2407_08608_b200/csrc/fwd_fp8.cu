@@ -14,6 +14,8 @@ int launch_fwd_fp8(const fa3b_fwd_params& p, cudaStream_t s) {
   constexpr int K = KIND_E4M3;
   if (p.schedule == FA3B_SCHED_NO_WS) return FA3B_ERR_SCHEDULE;
   switch (p.head_dim) {
+    case 64:  // 64-byte rows: 64-byte swizzle; the pair with three rotating S buffers (S3)
+      return launch_fwd_fp8_d64(p, s);
     case 128:
       switch (p.schedule) {
         case FA3B_SCHED_BASIC: return launch_fwd_c<128, 1, 1, SCHED_SERIAL, K>(p, s);
@@ -30,7 +32,7 @@ int launch_fwd_fp8(const fa3b_fwd_params& p, cudaStream_t s) {
       }
       return launch_fwd_c<256, 1, 1, SCHED_DEFAULT, K>(p, s);  // = 3-stage (S2)
   }
-  return FA3B_ERR_HEAD_DIM;  // e4m3 rows of 64 bytes would need a 64B swizzle
+  return FA3B_ERR_HEAD_DIM;
 }
 
 }  // namespace fa3b

@@ -82,6 +82,9 @@
 #ifndef FA3B_FWD_OREGS
 #define FA3B_FWD_OREGS 56
 #endif
+#ifndef FA3B_FWD_PSPLIT
+#define FA3B_FWD_PSPLIT 0
+#endif
 
 namespace fa3b {
 
@@ -172,9 +175,14 @@ struct FwdTraits {
   static_assert(SCHED == SCHED_DEFAULT || (NT == 1 && CPS == 1), "schedule variants are one-tile");
   static constexpr int BM = 128;
   static constexpr int BN = 128;
-  static constexpr int CHUNK_BYTES = 128 * 128;  // 128 rows x 128 bytes
-  static constexpr int CHUNK_ELEMS = 128 / EB;
+  // smem tiles are CHUNKS column chunks of 128 rows x ROW_BYTES, swizzled by the
+  // row width: 128 bytes, or 64 (e4m3 at d = 64, 64-byte swizzle)
+  static constexpr int ROW_BYTES = D * EB < 128 ? D * EB : 128;
+  static constexpr int CHUNK_BYTES = 128 * ROW_BYTES;
+  static constexpr int CHUNK_ELEMS = ROW_BYTES / EB;
   static constexpr int CHUNKS = D / CHUNK_ELEMS;
+  static constexpr int KPR = ROW_BYTES / 32;       // 32-byte MMA K steps per row chunk
+  static constexpr int SBO = 8 * ROW_BYTES;        // stride of 8-row swizzle atoms
   static constexpr int TILE_BYTES = CHUNKS * CHUNK_BYTES;
   static constexpr int STAGES = CPS == 2 ? (TILE_BYTES <= 16384 ? 4 : 2)
                                          : (TILE_BYTES <= 16384 ? 8 : (TILE_BYTES <= 32768 ? 4 : 2));
@@ -289,9 +297,9 @@ struct NowsLeader {
     constexpr int KSTEP = 32 / T::EB;
 #pragma unroll
     for (int k = 0; k < T::D / KSTEP; ++k) {
-      const uint32_t off = (k >> 2) * T::CHUNK_BYTES + (k & 3) * 32;
-      const uint64_t a = ptx::sw128_desc(q_addr + off, 16, 1024);
-      const uint64_t bd = ptx::sw128_desc(kv_addr + slot * T::TILE_BYTES + off, 16, 1024);
+      const uint32_t off = (k / T::KPR) * T::CHUNK_BYTES + (k % T::KPR) * 32;
+      const uint64_t a = ptx::swz_desc<T::ROW_BYTES>(q_addr + off, 16, T::SBO);
+      const uint64_t bd = ptx::swz_desc<T::ROW_BYTES>(kv_addr + slot * T::TILE_BYTES + off, 16, T::SBO);
       if constexpr (FP8)
         ptx::mma_f8_ss(tmem + T::s2_col(gs & 1), a, bd, idesc_qk, k > 0 ? 1u : 0u);
       else
@@ -330,8 +338,8 @@ struct NowsLeader {
     const uint32_t scol = T::s2_col((g0 + j) & 1);
 #pragma unroll
     for (int k = 0; k < 128 / KSTEP; ++k) {
-      const uint64_t bd = ptx::sw128_desc(kv_addr + slot * T::TILE_BYTES + k * KSTEP * 128,
-                                          T::CHUNK_BYTES, 1024);
+      const uint64_t bd = ptx::swz_desc<T::ROW_BYTES>(kv_addr + slot * T::TILE_BYTES + k * KSTEP * T::ROW_BYTES,
+                                                      T::CHUNK_BYTES, T::SBO);
       if constexpr (FP8)
         ptx::mma_f8_ts(tmem + T::o_col(0), tmem + scol + k * 8, bd, idesc_pv,
                        (j > 0 || k > 0) ? 1u : 0u);
@@ -528,9 +536,9 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       auto issue_qk = [&](int t, int slot, int scol) {
 #pragma unroll
         for (int k = 0; k < D / KSTEP; ++k) {
-          const uint32_t off = (k >> 2) * T::CHUNK_BYTES + (k & 3) * 32;
-          const uint64_t a = ptx::sw128_desc(q_addr + t * T::TILE_BYTES + off, 16, 1024);
-          const uint64_t bd = ptx::sw128_desc(kv_addr + slot * T::TILE_BYTES + off, 16, 1024);
+          const uint32_t off = (k / T::KPR) * T::CHUNK_BYTES + (k % T::KPR) * 32;
+          const uint64_t a = ptx::swz_desc<T::ROW_BYTES>(q_addr + t * T::TILE_BYTES + off, 16, T::SBO);
+          const uint64_t bd = ptx::swz_desc<T::ROW_BYTES>(kv_addr + slot * T::TILE_BYTES + off, 16, T::SBO);
           if constexpr (FP8)
             ptx::mma_f8_ss(tmem + scol, a, bd, idesc_qk, k > 0 ? 1u : 0u);
           else
@@ -540,9 +548,9 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       auto issue_pv = [&](int t, int slot, bool acc, int scol) {
 #pragma unroll
         for (int k = 0; k < 128 / KSTEP; ++k) {
-          // B = V, MN-major: KSTEP kv rows of 128 bytes per step
-          const uint64_t bd = ptx::sw128_desc(kv_addr + slot * T::TILE_BYTES + k * KSTEP * 128,
-                                              T::CHUNK_BYTES, 1024);
+          // B = V, MN-major: KSTEP kv rows of ROW_BYTES per step
+          const uint64_t bd = ptx::swz_desc<T::ROW_BYTES>(
+              kv_addr + slot * T::TILE_BYTES + k * KSTEP * T::ROW_BYTES, T::CHUNK_BYTES, T::SBO);
           // A = P in TMEM: KSTEP elements = 8 columns of 32 bits
           if constexpr (FP8)
             ptx::mma_f8_ts(tmem + T::o_col(t), tmem + scol + k * 8, bd, idesc_pv,
@@ -560,7 +568,8 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
         uint32_t ta[KS];
 #pragma unroll
         for (int k = 0; k < KS; ++k) {
-          bd[k] = ptx::sw128_desc(kv_addr + slot * T::TILE_BYTES + k * KSTEP * 128, T::CHUNK_BYTES, 1024);
+          bd[k] = ptx::swz_desc<T::ROW_BYTES>(kv_addr + slot * T::TILE_BYTES + k * KSTEP * T::ROW_BYTES,
+                                              T::CHUNK_BYTES, T::SBO);
           ta[k] = tmem + scol + k * 8;
           asm volatile("" : "+l"(bd[k]), "+r"(ta[k]));
         }
@@ -937,6 +946,17 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
           } else {
             pk[i] = BF16 ? ptx::pack_bf16(pp.x, pp.y) : ptx::pack_f16(pp.x, pp.y);
           }
+          // PSPLIT: the first half of P goes to TMEM as soon as it is packed, which
+          // frees its registers for the second half (the exchange barrier has already
+          // ordered every split's S load before these stores)
+          if constexpr (FA3B_FWD_PSPLIT && NPK >= 16) {
+            if (i == HC / 4 - 1) {
+              if constexpr (NPK == 16)
+                ptx::tmem_st8(tS + NPK * hh, *reinterpret_cast<uint32_t(*)[8]>(&pk[0]));
+              else
+                ptx::tmem_st16(tS + NPK * hh, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
+            }
+          }
         }
         const float2 a4 = __fadd2_rn(__fadd2_rn(acc[0], acc[1]), __fadd2_rn(acc[2], acc[3]));
         psum = a4.x + a4.y;
@@ -953,12 +973,18 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       exp_half((m_cur == -INFINITY) ? 0.f : m_cur);
       // P (packed, key order) over the first columns of this block's S buffer; every
       // split's S load has completed (the exchange barrier above)
-      if constexpr (NPK == 8)
+      if constexpr (FA3B_FWD_PSPLIT && NPK >= 16) {
+        if constexpr (NPK == 16)
+          ptx::tmem_st8(tS + NPK * hh + 8, *reinterpret_cast<uint32_t(*)[8]>(&pk[8]));
+        else
+          ptx::tmem_st16(tS + NPK * hh + 16, *reinterpret_cast<uint32_t(*)[16]>(&pk[16]));
+      } else if constexpr (NPK == 8) {
         ptx::tmem_st8(tS + NPK * hh, *reinterpret_cast<uint32_t(*)[8]>(&pk[0]));
-      else if constexpr (NPK == 16)
+      } else if constexpr (NPK == 16) {
         ptx::tmem_st16(tS + NPK * hh, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
-      else
+      } else {
         ptx::tmem_st32(tS + NPK * hh, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+      }
       l = l * factor + psum * (inv_pmul * inv_rho);
       if (tr) FA3B_TP(t, j, 4);
       const float ofac = factor * vfac;

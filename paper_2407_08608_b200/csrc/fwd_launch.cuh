@@ -50,12 +50,13 @@ int launch_fwd(const fa3b_fwd_params& p, cudaStream_t stream) {
   int rc = ensure_smem_attr(reinterpret_cast<const void*>(kern), T::SMEM_BYTES);
   if (rc != FA3B_OK) return rc;
   CUtensorMap tq, tk, tv;
-  const int box = FP8 ? 128 : 64;  // 128-byte rows of the swizzled tiles
-  if ((rc = make_tmap_4d(&tq, p.q, EB, D, p.heads_q, p.seqlen, p.batch, box, 128)) != FA3B_OK)
+  const int box = T::CHUNK_ELEMS;  // ROW_BYTES-wide rows of the swizzled tiles
+  const int swz = T::ROW_BYTES;
+  if ((rc = make_tmap_4d(&tq, p.q, EB, D, p.heads_q, p.seqlen, p.batch, box, 128, swz)) != FA3B_OK)
     return rc;
-  if ((rc = make_tmap_4d(&tk, p.k, EB, D, p.heads_kv, p.seqlen, p.batch, box, 128)) != FA3B_OK)
+  if ((rc = make_tmap_4d(&tk, p.k, EB, D, p.heads_kv, p.seqlen, p.batch, box, 128, swz)) != FA3B_OK)
     return rc;
-  if ((rc = make_tmap_4d(&tv, p.v, EB, D, p.heads_kv, p.seqlen, p.batch, box, 128)) != FA3B_OK)
+  if ((rc = make_tmap_4d(&tv, p.v, EB, D, p.heads_kv, p.seqlen, p.batch, box, 128, swz)) != FA3B_OK)
     return rc;
   FwdArgs a;
   a.B = p.batch;

@@ -356,6 +356,26 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t smem_addr, uint32_t lbo,
   return d;
 }
 
+// 64-byte swizzle (rows of 64 bytes: e4m3 at d = 64; 8-row atoms of 512 bytes)
+__device__ __forceinline__ uint64_t sw64_desc(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr & 0x3FFFFu) >> 4);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= 1ull << 46;  // descriptor version for sm_100
+  d |= 4ull << 61;  // SWIZZLE_64B
+  return d;
+}
+// the swizzle that matches a tile's row width (128 or 64 bytes)
+template <int ROW_BYTES>
+__device__ __forceinline__ uint64_t swz_desc(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
+  static_assert(ROW_BYTES == 128 || ROW_BYTES == 64, "row width");
+  if constexpr (ROW_BYTES == 128)
+    return sw128_desc(smem_addr, lbo, sbo);
+  else
+    return sw64_desc(smem_addr, lbo, sbo);
+}
+
 // Instruction descriptor for kind::f16 (fmt 0 = f16, 1 = bf16) and
 // kind::f8f6f4 (fmt 0 = e4m3), fp32 accumulate.
 __host__ __device__ constexpr uint32_t make_idesc(uint32_t m, uint32_t n, uint32_t a_fmt,

@@ -80,7 +80,8 @@ def _fp8_case(port, ref, cuda, N, D, causal, seed, tile=128):
 
 
 @pytest.mark.parametrize("N,D,causal", [(1024, 128, False), (1024, 128, True), (640, 256, False),
-                                        (1000, 256, True)])
+                                        (1000, 256, True), (1024, 64, False), (1000, 64, True),
+                                        (300, 64, False)])
 def test_fp8_fwd_error_band(port, cuda, N, D, causal):
     o, lse, o_ref, l_ref, o_emu, l_emu, *_ = _fp8_case(port, None, cuda, N, D, causal,
                                                         seed=N + D)
@@ -143,7 +144,10 @@ def test_fp8_rejects_bad_blocks(cuda):
 
 @pytest.mark.parametrize("B,N,H,D,causal,per_block", [(1, 16384, 8, 256, False, True),
                                                       (2, 4173, 8, 256, True, True),
-                                                      (1, 16384, 8, 256, False, False)])
+                                                      (1, 16384, 8, 256, False, False),
+                                                      (1, 8192, 16, 64, False, True),
+                                                      (2, 4173, 4, 64, True, True),
+                                                      (1, 8192, 16, 64, True, False)])
 def test_fp8_one_tile_many_items(cuda, B, N, H, D, causal, per_block):
     """K6 at d256 runs one query tile per CTA with a second S buffer in TMEM: many work
     items per persistent CTA, ragged causal blocks, both scale granularities (no
@@ -183,7 +187,11 @@ def test_fp8_one_tile_many_items(cuda, B, N, H, D, causal, per_block):
             emu = ((p * 448).to(e4m3).float() / 448) @ quant(vf) / p.sum(-1, keepdim=True)
             err, err_emu = (o[b, rows, h] - ref).norm().item(), (emu - ref).norm().item()
             assert err <= 1.3 * err_emu + 1e-3 * ref.norm().item(), (err, err_emu)
-            assert (lse[b, h, rows] - torch.logsumexp(s, -1)).abs().max().item() < 0.05
+            # LSE: the kernel's scores are the e4m3 ones (tight), which differ from the
+            # exact scores by the quantization error (loose: per tensor at d 64 a single
+            # causal score moves by up to ~0.07)
+            assert (lse[b, h, rows] - torch.logsumexp(s8, -1)).abs().max().item() < 0.01
+            assert (lse[b, h, rows] - torch.logsumexp(s, -1)).abs().max().item() < 0.1
 
 
 def _bf16_rows(kind, N, D, rng):
