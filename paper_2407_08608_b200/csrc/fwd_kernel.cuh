@@ -82,6 +82,9 @@
 #ifndef FA3B_FWD_OREGS
 #define FA3B_FWD_OREGS 56
 #endif
+#ifndef FA3B_MMA_SPIN
+#define FA3B_MMA_SPIN 0
+#endif
 #ifndef FA3B_FWD_PSPLIT
 #define FA3B_FWD_PSPLIT 0
 #endif
@@ -574,7 +577,11 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
           asm volatile("" : "+l"(bd[k]), "+r"(ta[k]));
         }
         const uint32_t to = tmem + T::o_col(t);
+#if FA3B_MMA_SPIN
+        ptx::mbar_wait_spin(p_bar, par);
+#else
         ptx::mbar_wait(p_bar, par);
+#endif
         ptx::tc_fence_after();
 #pragma unroll
         for (int k = 0; k < KS; ++k) {

@@ -104,6 +104,12 @@ __device__ __forceinline__ bool mbar_try_wait_sleep(uint32_t bar, uint32_t parit
       : "memory");
   return ok != 0;
 }
+// Spinning variant (no suspend) for a latency-critical single waiter.
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  while (!mbar_try_wait(a, parity)) {
+  }
+}
 // Blocks until the phase with the given parity has completed. With the
 // watchdog on, a wait that exceeds ~2^34 cycles (several seconds) traps so a
 // protocol bug surfaces as a launch error instead of a hung device.
