@@ -165,19 +165,28 @@ enum FwdSched {
 // NQ_ = column splits of a query tile over its softmax warpgroups: 2 (two
 // warpgroups, 64 S columns per thread) or 4 (four warpgroups, 32 columns per
 // thread: half the per-thread softmax chain, for the one-tile S2 schedule).
-template <int D_, int NT_, int EB_ = 2, int CPS_ = 1, int SCHED_ = SCHED_DEFAULT, int NQ_ = 2>
+// BN_ = keys per KV block: 128, or 64 for the P2 pair (NT = 2, NQ = 1: one softmax
+// warpgroup per query tile, thread = row, and two 64-column S buffers per tile, so
+// S(t, j + 2) is computed while the softmax works on block j + 1 — the S2 overlap
+// for both tiles of the pair within the 512 TMEM columns).
+template <int D_, int NT_, int EB_ = 2, int CPS_ = 1, int SCHED_ = SCHED_DEFAULT, int NQ_ = 2,
+          int BN_ = 128>
 struct FwdTraits {
   static constexpr int D = D_;
   static constexpr int NT = NT_;
   static constexpr int NQ = NQ_;
-  static_assert(NQ == 2 || (NQ == 4 && NT_ == 1 && CPS_ == 1 && SCHED_ != SCHED_NOWS), "NQ = 4 is one-tile");
+  static constexpr int BN = BN_;
+  static constexpr bool P2 = BN == 64;
+  static_assert(BN == 128 || (BN == 64 && NT_ == 2 && CPS_ == 1 && SCHED_ == SCHED_DEFAULT && NQ_ == 1),
+                "BN = 64 is the P2 pair");
+  static_assert(NQ == 2 || (NQ == 4 && NT_ == 1 && CPS_ == 1 && SCHED_ != SCHED_NOWS) || (NQ == 1 && P2),
+                "NQ = 4 is one-tile, NQ = 1 the P2 pair");
   static constexpr int WPT = 4 * NQ;  // softmax warps per query tile
   static constexpr int EB = EB_;  // bytes per element (2 f16/bf16, 1 e4m3)
   static constexpr int CPS = CPS_;
   static constexpr int SCHED = SCHED_;
   static_assert(SCHED == SCHED_DEFAULT || (NT == 1 && CPS == 1), "schedule variants are one-tile");
   static constexpr int BM = 128;
-  static constexpr int BN = 128;
   // smem tiles are CHUNKS column chunks of 128 rows x ROW_BYTES, swizzled by the
   // row width: 128 bytes, or 64 (e4m3 at d = 64, 64-byte swizzle)
   static constexpr int ROW_BYTES = D * EB < 128 ? D * EB : 128;
@@ -186,9 +195,11 @@ struct FwdTraits {
   static constexpr int CHUNKS = D / CHUNK_ELEMS;
   static constexpr int KPR = ROW_BYTES / 32;       // 32-byte MMA K steps per row chunk
   static constexpr int SBO = 8 * ROW_BYTES;        // stride of 8-row swizzle atoms
-  static constexpr int TILE_BYTES = CHUNKS * CHUNK_BYTES;
-  static constexpr int STAGES = CPS == 2 ? (TILE_BYTES <= 16384 ? 4 : 2)
-                                         : (TILE_BYTES <= 16384 ? 8 : (TILE_BYTES <= 32768 ? 4 : 2));
+  static constexpr int TILE_BYTES = CHUNKS * CHUNK_BYTES;        // a 128-row Q tile
+  static constexpr int KV_CHUNK_BYTES = BN * ROW_BYTES;           // a BN-row K/V column chunk
+  static constexpr int KV_TILE_BYTES = CHUNKS * KV_CHUNK_BYTES;   // a K or V block
+  static constexpr int STAGES = CPS == 2 ? (KV_TILE_BYTES <= 16384 ? 4 : 2)
+                                         : (KV_TILE_BYTES <= 16384 ? 8 : (KV_TILE_BYTES <= 32768 ? 4 : 2));
   // no warp specialization: the softmax warps issue loads and MMAs themselves
   static constexpr bool NOWS = SCHED == SCHED_NOWS;
   static_assert(!NOWS || STAGES >= 4, "no-WS schedule needs a 4-stage K/V ring");
@@ -206,11 +217,11 @@ struct FwdTraits {
   static_assert(!S2 || 2 * 128 + D <= 512, "S2 TMEM budget");
   // d = 64 tile pair: three S buffers rotate between the two tiles (3 x 128 + 2 x 64
   // columns), so each tile's next S is computed during its softmax (see the header)
-  static constexpr bool S3 = NT == 2 && D == 64 && CPS == 1 && FA3B_FWD_S3;
+  static constexpr bool S3 = NT == 2 && D == 64 && CPS == 1 && FA3B_FWD_S3 && !P2;
   static_assert(!S3 || 3 * 128 + 2 * D <= 512, "S3 TMEM budget");
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_KV = NT * TILE_BYTES;
-  static constexpr int OFF_BAR = OFF_KV + STAGES * TILE_BYTES;
+  static constexpr int OFF_BAR = OFF_KV + STAGES * KV_TILE_BYTES;
   // q_full, kv_full[S], kv_empty[S], s_full[2 NT], p_full[NT], o_full[NT], q_empty,
   // pv_done[NT] (the second s_full per tile and pv_done serve S2 / S3)
   static constexpr int NUM_BARS = 3 + 2 * STAGES + 5 * NT;
@@ -218,11 +229,16 @@ struct FwdTraits {
   static constexpr int OFF_XCH = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr int SMEM_BYTES = OFF_XCH + NT * 2 * NQ * 128 * 4 + 1024;
   static_assert(NT * (128 + D) <= static_cast<int>(TMEM_COLS), "TMEM budget");
+  static_assert(!P2 || NT * (2 * BN + D) <= 512, "P2 TMEM budget");
   static_assert(CPS == 1 || (NT == 1 && SMEM_BYTES * 2 <= 233472), "two CTAs per SM");
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
   __host__ __device__ static constexpr int s_col(int t) { return t * 128; }
   __host__ __device__ static constexpr int s2_col(int buf) { return buf ? 128 + D : 0; }
-  __host__ __device__ static constexpr int o_col(int t) { return (S3 ? 384 : NT * 128) + t * D; }
+  // P2: tile t's S buffer b at (2 t + b) BN, O after the four buffers
+  __host__ __device__ static constexpr int p2_col(int t, int b) { return (2 * t + b) * BN; }
+  __host__ __device__ static constexpr int o_col(int t) {
+    return (S3 ? 384 : (P2 ? NT * 2 * BN : NT * 128)) + t * D;
+  }
 };
 
 // SCHED_NOWS: the producer and MMA-issuer work of the one-tile S2 schedule, done
@@ -278,10 +294,10 @@ struct NowsLeader {
       }
       const int slot = lpos % T::STAGES;
       ptx::mbar_wait(&kv_empty[slot], ((lpos / T::STAGES) & 1) ^ 1);
-      ptx::mbar_arrive_expect_tx(&kv_full[slot], T::TILE_BYTES);
+      ptx::mbar_arrive_expect_tx(&kv_full[slot], T::KV_TILE_BYTES);
 #pragma unroll
       for (int c = 0; c < T::CHUNKS; ++c)
-        ptx::tma_load_4d(smem + T::OFF_KV + slot * T::TILE_BYTES + c * T::CHUNK_BYTES,
+        ptx::tma_load_4d(smem + T::OFF_KV + slot * T::KV_TILE_BYTES + c * T::KV_CHUNK_BYTES,
                          is_v ? tmV : tmK, &kv_full[slot], c * T::CHUNK_ELEMS, it_hkv, blk * 128,
                          it_b, ptx::kEvictLast);
       ++lpos;
@@ -301,8 +317,9 @@ struct NowsLeader {
 #pragma unroll
     for (int k = 0; k < T::D / KSTEP; ++k) {
       const uint32_t off = (k / T::KPR) * T::CHUNK_BYTES + (k % T::KPR) * 32;
+      const uint32_t offb = (k / T::KPR) * T::KV_CHUNK_BYTES + (k % T::KPR) * 32;
       const uint64_t a = ptx::swz_desc<T::ROW_BYTES>(q_addr + off, 16, T::SBO);
-      const uint64_t bd = ptx::swz_desc<T::ROW_BYTES>(kv_addr + slot * T::TILE_BYTES + off, 16, T::SBO);
+      const uint64_t bd = ptx::swz_desc<T::ROW_BYTES>(kv_addr + slot * T::KV_TILE_BYTES + offb, 16, T::SBO);
       if constexpr (FP8)
         ptx::mma_f8_ss(tmem + T::s2_col(gs & 1), a, bd, idesc_qk, k > 0 ? 1u : 0u);
       else
@@ -340,9 +357,9 @@ struct NowsLeader {
     constexpr int KSTEP = 32 / T::EB;
     const uint32_t scol = T::s2_col((g0 + j) & 1);
 #pragma unroll
-    for (int k = 0; k < 128 / KSTEP; ++k) {
-      const uint64_t bd = ptx::swz_desc<T::ROW_BYTES>(kv_addr + slot * T::TILE_BYTES + k * KSTEP * T::ROW_BYTES,
-                                                      T::CHUNK_BYTES, T::SBO);
+    for (int k = 0; k < T::BN / KSTEP; ++k) {
+      const uint64_t bd = ptx::swz_desc<T::ROW_BYTES>(
+          kv_addr + slot * T::KV_TILE_BYTES + k * KSTEP * T::ROW_BYTES, T::KV_CHUNK_BYTES, T::SBO);
       if constexpr (FP8)
         ptx::mma_f8_ts(tmem + T::o_col(0), tmem + scol + k * 8, bd, idesc_pv,
                        (j > 0 || k > 0) ? 1u : 0u);
@@ -364,15 +381,15 @@ struct NowsLeader {
 #endif
 
 template <int D, int NT, bool CAUSAL, int KIND, int CPS = 1, int EMU = FA3B_FWD_EMU,
-          int SCHED = SCHED_DEFAULT, int NQ = 2>
-__global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CPS, SCHED, NQ>::NUM_THREADS, CPS)
+          int SCHED = SCHED_DEFAULT, int NQ = 2, int BN = 128>
+__global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CPS, SCHED, NQ, BN>::NUM_THREADS, CPS)
     fa3b_fwd_kernel(const __grid_constant__ CUtensorMap tmQ,
                     const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const FwdArgs args,
                     const uint32_t idesc_qk, const uint32_t idesc_pv) {
   constexpr bool FP8 = KIND == KIND_E4M3;
   constexpr bool BF16 = KIND == KIND_BF16;
-  using T = FwdTraits<D, NT, FP8 ? 1 : 2, CPS, SCHED, NQ>;
+  using T = FwdTraits<D, NT, FP8 ? 1 : 2, CPS, SCHED, NQ, BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -405,7 +422,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
 #define nqb ((fwd_seqlen(args) + NT * 128 - 1) / (NT * 128))
 #define HB (args.H * args.B)
 #define num_items (nqb * HB)
-#define nkv ((fwd_seqlen(args) + 127) / 128)
+#define nkv ((fwd_seqlen(args) + T::BN - 1) / T::BN)
   struct Item {
     int qb, h, b, hkv, q_base, n_max;
     int n_t[NT];
@@ -428,7 +445,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
       const int r0 = w.q_base + t * 128;
-      w.n_t[t] = (r0 < N) ? (CAUSAL ? min(nkv, r0 / 128 + 1) : nkv) : 0;
+      w.n_t[t] = (r0 < N) ? (CAUSAL ? min(nkv, (r0 + 128) / T::BN) : nkv) : 0;
       w.n_max = max(w.n_max, w.n_t[t]);
     }
     return w;
@@ -498,15 +515,15 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
           const int slot = item % T::STAGES;
           const uint32_t ph = (item / T::STAGES) & 1;
           ptx::mbar_wait(&kv_empty[slot], ph ^ 1);
-          ptx::mbar_arrive_expect_tx(&kv_full[slot], T::TILE_BYTES);
-          uint8_t* dst = smem + T::OFF_KV + slot * T::TILE_BYTES;
+          ptx::mbar_arrive_expect_tx(&kv_full[slot], T::KV_TILE_BYTES);
+          uint8_t* dst = smem + T::OFF_KV + slot * T::KV_TILE_BYTES;
 #pragma unroll
           for (int c = 0; c < T::CHUNKS; ++c)
-            ptx::tma_load_4d(dst + c * T::CHUNK_BYTES, is_v ? &tmV : &tmK, &kv_full[slot],
-                             c * T::CHUNK_ELEMS, w.hkv, blk * 128, w.b, ptx::kEvictLast);
+            ptx::tma_load_4d(dst + c * T::KV_CHUNK_BYTES, is_v ? &tmV : &tmK, &kv_full[slot],
+                             c * T::CHUNK_ELEMS, w.hkv, blk * T::BN, w.b, ptx::kEvictLast);
           ++item;
         };
-        if constexpr (T::S2 || T::S3) {
+        if constexpr (T::S2 || T::S3 || T::P2) {
           // the MMA warp's order: K_0, K_1, { V_j, K_{j+2} }_j
           const int n = w.n_max;
           load_kv(false, 0);
@@ -540,8 +557,9 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
 #pragma unroll
         for (int k = 0; k < D / KSTEP; ++k) {
           const uint32_t off = (k / T::KPR) * T::CHUNK_BYTES + (k % T::KPR) * 32;
+          const uint32_t offb = (k / T::KPR) * T::KV_CHUNK_BYTES + (k % T::KPR) * 32;
           const uint64_t a = ptx::swz_desc<T::ROW_BYTES>(q_addr + t * T::TILE_BYTES + off, 16, T::SBO);
-          const uint64_t bd = ptx::swz_desc<T::ROW_BYTES>(kv_addr + slot * T::TILE_BYTES + off, 16, T::SBO);
+          const uint64_t bd = ptx::swz_desc<T::ROW_BYTES>(kv_addr + slot * T::KV_TILE_BYTES + offb, 16, T::SBO);
           if constexpr (FP8)
             ptx::mma_f8_ss(tmem + scol, a, bd, idesc_qk, k > 0 ? 1u : 0u);
           else
@@ -550,10 +568,10 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       };
       auto issue_pv = [&](int t, int slot, bool acc, int scol) {
 #pragma unroll
-        for (int k = 0; k < 128 / KSTEP; ++k) {
+        for (int k = 0; k < T::BN / KSTEP; ++k) {
           // B = V, MN-major: KSTEP kv rows of ROW_BYTES per step
           const uint64_t bd = ptx::swz_desc<T::ROW_BYTES>(
-              kv_addr + slot * T::TILE_BYTES + k * KSTEP * T::ROW_BYTES, T::CHUNK_BYTES, T::SBO);
+              kv_addr + slot * T::KV_TILE_BYTES + k * KSTEP * T::ROW_BYTES, T::KV_CHUNK_BYTES, T::SBO);
           // A = P in TMEM: KSTEP elements = 8 columns of 32 bits
           if constexpr (FP8)
             ptx::mma_f8_ts(tmem + T::o_col(t), tmem + scol + k * 8, bd, idesc_pv,
@@ -566,13 +584,13 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       // PV with its operand descriptors computed before the wait for P (pinned by an
       // empty asm so they are not sunk below it): only the MMA issue follows P
       auto issue_pv_pre = [&](int t, int slot, bool acc, int scol, uint64_t* p_bar, uint32_t par) {
-        constexpr int KS = 128 / KSTEP;
+        constexpr int KS = T::BN / KSTEP;
         uint64_t bd[KS];
         uint32_t ta[KS];
 #pragma unroll
         for (int k = 0; k < KS; ++k) {
-          bd[k] = ptx::swz_desc<T::ROW_BYTES>(kv_addr + slot * T::TILE_BYTES + k * KSTEP * T::ROW_BYTES,
-                                              T::CHUNK_BYTES, T::SBO);
+          bd[k] = ptx::swz_desc<T::ROW_BYTES>(kv_addr + slot * T::KV_TILE_BYTES + k * KSTEP * T::ROW_BYTES,
+                                              T::KV_CHUNK_BYTES, T::SBO);
           ta[k] = tmem + scol + k * 8;
           asm volatile("" : "+l"(bd[k]), "+r"(ta[k]));
         }
@@ -705,6 +723,63 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
           kvi += 2 * n;
           gb += 2 * n;
         }
+      } else if constexpr (T::P2) {
+        // Two tiles, two BN-column S buffers each (tile t's S number g in buffer g & 1).
+        // Per item: S(0,0) ; S(1,0) ; S(0,1) ; S(1,1) ;
+        //   { PV(0,j) ; S(0,j+2) ; PV(1,j) ; S(1,j+2) }_j
+        // S(t, j+2) reuses the buffer of S(t, j) = P(t, j), issued right after the PV
+        // that reads it, so each tile's next S is always one block ahead of its softmax.
+        int sn[NT] = {};   // S GEMMs issued per tile
+        int pn[NT] = {};   // PV GEMMs issued per tile (P(t, j) in buffer pn & 1)
+        auto s_issue = [&](int t, int slot) {
+          issue_qk(t, slot, T::p2_col(t, sn[t] & 1));
+          ptx::mma_commit(&s_full[2 * t + (sn[t] & 1)]);
+          ++sn[t];
+        };
+        for (int lin = item_of(0); lin < num_items; lin = item_of(++itl)) {
+          const Item w = decode(lin);
+          const int n0 = w.n_t[0], n1 = w.n_t[1], n = w.n_max;
+          ptx::mbar_wait(q_full, itl & 1);
+          int pos = kvi;  // ring position, producer order K_0, K_1, {V_j, K_{j+2}}
+          auto wait_pos = [&]() {
+            ptx::mbar_wait(&kv_full[pos % T::STAGES], (pos / T::STAGES) & 1);
+            ptx::tc_fence_after();
+            return pos++ % T::STAGES;
+          };
+          for (int j = 0; j < 2 && j < n; ++j) {
+            const int slot = wait_pos();
+            if (j < n0) s_issue(0, slot);
+            if (j < n1) s_issue(1, slot);
+            ptx::mma_commit(&kv_empty[slot]);
+          }
+          for (int j = 0; j < n; ++j) {
+            const int slot_v = wait_pos();
+            // K_{j+2}'s ring entry, waited for only when its first S is issued
+            const int kpos = j + 2 < n ? pos++ : -1;
+            bool k_ready = false;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+              if (j < w.n_t[t]) {
+                issue_pv_pre(t, slot_v, j > 0, T::p2_col(t, pn[t] & 1), &p_full[t], pc[t]++ & 1);
+                ++pn[t];
+                ptx::mma_commit(&pv_done[t]);
+                if (j + 1 == w.n_t[t]) ptx::mma_commit(&o_full[t]);
+              }
+              if (j + 2 < w.n_t[t]) {
+                if (!k_ready) {
+                  ptx::mbar_wait(&kv_full[kpos % T::STAGES], (kpos / T::STAGES) & 1);
+                  ptx::tc_fence_after();
+                  k_ready = true;
+                }
+                s_issue(t, kpos % T::STAGES);
+              }
+            }
+            ptx::mma_commit(&kv_empty[slot_v]);
+            if (kpos >= 0) ptx::mma_commit(&kv_empty[kpos % T::STAGES]);
+          }
+          ptx::mma_commit(q_empty);
+          kvi += 2 * n;
+        }
       } else
       for (int lin = item_of(0); lin < num_items; lin = item_of(++itl)) {
         const Item w = decode(lin);
@@ -783,7 +858,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
     if constexpr (T::NOWS)
       if (leader) nows.item_start(w.h, w.hkv, w.b, w.q_base, w.n_t[0], itl);
     const int nt = (t == 0) ? w.n_t[0] : w.n_t[NT - 1];
-    constexpr int HC = 128 / NQ;         // S columns per thread
+    constexpr int HC = T::BN / NQ;       // S columns per thread
     constexpr int DH = D / NQ;           // O columns per thread
     constexpr int CW = DH < 32 ? DH : 32;  // O columns per TMEM load / store
     auto tmem_ldw = [](uint32_t a, uint32_t (&v)[CW]) {
@@ -820,7 +895,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       // a tile past N (nt == 0, odd block count in the pair path) has no scale
       if (nt > 0)
         sl2 *= args.q_blocked ? args.q_scale[hq * nqb_all + q_base / 128 + t] : args.q_scale[hq];
-      ks_base = static_cast<int>(args.kv_blocked ? hk * nkv : hk);
+      ks_base = static_cast<int>(args.kv_blocked ? hk * nqb_all : hk);  // 128-row scale blocks
     }
     float v_cur = 0.f;  // V scale the O accumulator is expressed in (FP8)
     float m_use = -INFINITY;  // running max in use, scaled log2 units (same in both halves)
@@ -845,9 +920,9 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       if constexpr (FP8) {
         slj = sl2 * ks_next;
         const float vs = vs_next;
-        if (args.kv_blocked && j + 1 < nt) {
-          ks_next = ksp[j + 1];
-          vs_next = vsp[j + 1];
+        if (args.kv_blocked && j + 1 < nt) {  // scales are per 128-key block
+          ks_next = ksp[((j + 1) * T::BN) >> 7];
+          vs_next = vsp[((j + 1) * T::BN) >> 7];
         }
         if (vs != v_cur) {
           // O stays in units of v_cur while rho = s_v[j] / v_cur is an exact power of
@@ -873,15 +948,17 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       // 2-stage order (flash_fwd.cpp:148-169): softmax_j begins once PV_{j-1} is done
       if constexpr (T::TWO_STAGE)
         if (j > 0) ptx::mbar_wait(&pv_done[t], (sc - 1) & 1);
-      if constexpr (T::S2 || T::S3)
+      if constexpr (T::S2 || T::S3 || T::P2)
         ptx::mbar_wait(&s_full[2 * t + (sc & 1)], (sc >> 1) & 1);
       else
         ptx::mbar_wait(&s_full[2 * t], sc & 1);
       ++sc;
       // S2: S / P of this block live in buffer (sc - 1) & 1
       // S3: S(t, j) lives in buffer (item base + 2 j + t) % 3
+      // P2: S(t, j) lives in tile t's buffer (sc - 1) & 1
       const uint32_t tS = T::S2   ? tmem + lane_base + T::s2_col((sc - 1) & 1)
                           : T::S3 ? tmem + lane_base + 128 * ((gbase + 2 * j + t) % 3)
+                          : T::P2 ? tmem + lane_base + T::p2_col(t, (sc - 1) & 1)
                                   : tS0;
       if (tr) FA3B_TP(t, j, 1);
 #ifdef FA3B_TRACE
@@ -889,8 +966,8 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
 #endif
       ptx::tc_fence_after();
       float s[HC];
-      const int kv0 = j * 128 + HC * hh;
-      const bool need_mask = (j * 128 + 128 > N) || (CAUSAL && j == nt - 1);
+      const int kv0 = j * T::BN + HC * hh;
+      const bool need_mask = (j * T::BN + T::BN > N) || (CAUSAL && j * T::BN + T::BN - 1 > q_base + t * 128);
       auto load_s = [&]() {
         uint32_t sr[HC];
 #pragma unroll
@@ -922,7 +999,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       const float pm = fmaxf(ptx::max3(a0, a1, a2), a3);
       float* xb = xch + (xc & 1) * (NQ * 128);
       ++xc;
-      ptx::sts_f32(xb + hh * 128 + r, pm);
+      if constexpr (NQ > 1) ptx::sts_f32(xb + hh * 128 + r, pm);
       // P = 2^(s * slj - msub) for this half: FFMA2 pairs; EMU of every 8 pairs go
       // through the FMA-pipe polynomial, the rest through MUFU.EX2; FADD2 sums.
       constexpr int NPK = FP8 ? HC / 4 : HC / 2;
@@ -968,7 +1045,9 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
         const float2 a4 = __fadd2_rn(__fadd2_rn(acc[0], acc[1]), __fadd2_rn(acc[2], acc[3]));
         psum = a4.x + a4.y;
       };
-      ptx::named_bar_sync(bar_id, NQ * 128);  // also: every S load of this tile has completed
+      // also: every split's S load of this tile has completed (NQ = 1: a thread's own
+      // tcgen05.wait::ld orders its S load before its P store)
+      if constexpr (NQ > 1) ptx::named_bar_sync(bar_id, NQ * 128);
       float mx = pm;
 #pragma unroll
       for (int q = 1; q < NQ; ++q) mx = fmaxf(mx, ptx::lds_f32(xb + ((hh + q) % NQ) * 128 + r));
@@ -998,7 +1077,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       // S2: every iteration waits for PV(V_{j-1}) before handing over P_j, so one
       // PV is in flight at a time and the pv_done parity never skips a phase (a
       // wait only when O needs rescaling hung at bf16 d = 256)
-      if constexpr ((T::S2 || T::S3) && !T::TWO_STAGE)
+      if constexpr ((T::S2 || T::S3 || T::P2) && !T::TWO_STAGE)
         if (j > 0) ptx::mbar_wait(&pv_done[t], (sc - 2) & 1);
       // PV(V_{j-1}) is complete (see header / above); rescale this thread's O_t columns.
       if (j > 0 && __any_sync(0xffffffffu, ofac != 1.f)) rescale_o(ofac);
@@ -1015,8 +1094,10 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       // ---------------------------------------------------------- epilogue
       float* xb = xch + (xc & 1) * (NQ * 128);
       ++xc;
-      ptx::sts_f32(xb + hh * 128 + r, l);
-      ptx::named_bar_sync(bar_id, NQ * 128);
+      if constexpr (NQ > 1) {
+        ptx::sts_f32(xb + hh * 128 + r, l);
+        ptx::named_bar_sync(bar_id, NQ * 128);
+      }
       {
         // the row sum in a fixed order of the splits (the same in every thread of the row)
         float lt = 0.f;

@@ -38,15 +38,16 @@ inline float fp8_threshold(bool kv_blocked) {
   return kv_blocked ? 2.f : 4.f;
 }
 
-template <int D, int NT, bool CAUSAL, int KIND, int CPS = 1, int SCHED = SCHED_DEFAULT, int NQ = 2>
+template <int D, int NT, bool CAUSAL, int KIND, int CPS = 1, int SCHED = SCHED_DEFAULT, int NQ = 2,
+          int BN = 128>
 int launch_fwd(const fa3b_fwd_params& p, cudaStream_t stream) {
   constexpr bool FP8 = KIND == KIND_E4M3;
   constexpr int EB = FP8 ? 1 : 2;
-  using T = FwdTraits<D, NT, EB, CPS, SCHED, NQ>;
+  using T = FwdTraits<D, NT, EB, CPS, SCHED, NQ, BN>;
   // one-tile CTAs with S fetched early (S2) own the SM's MUFU: more of the exp2
   // pairs go to the FMA-pipe polynomial
   constexpr int EMU = T::S2 ? (FP8 ? FA3B_FWD_EMU_S2 : FA3B_FWD_EMU_S2_16) : FA3B_FWD_EMU;
-  auto kern = fa3b_fwd_kernel<D, NT, CAUSAL, KIND, CPS, EMU, SCHED, NQ>;
+  auto kern = fa3b_fwd_kernel<D, NT, CAUSAL, KIND, CPS, EMU, SCHED, NQ, BN>;
   int rc = ensure_smem_attr(reinterpret_cast<const void*>(kern), T::SMEM_BYTES);
   if (rc != FA3B_OK) return rc;
   CUtensorMap tq, tk, tv;
@@ -54,9 +55,9 @@ int launch_fwd(const fa3b_fwd_params& p, cudaStream_t stream) {
   const int swz = T::ROW_BYTES;
   if ((rc = make_tmap_4d(&tq, p.q, EB, D, p.heads_q, p.seqlen, p.batch, box, 128, swz)) != FA3B_OK)
     return rc;
-  if ((rc = make_tmap_4d(&tk, p.k, EB, D, p.heads_kv, p.seqlen, p.batch, box, 128, swz)) != FA3B_OK)
+  if ((rc = make_tmap_4d(&tk, p.k, EB, D, p.heads_kv, p.seqlen, p.batch, box, BN, swz)) != FA3B_OK)
     return rc;
-  if ((rc = make_tmap_4d(&tv, p.v, EB, D, p.heads_kv, p.seqlen, p.batch, box, 128, swz)) != FA3B_OK)
+  if ((rc = make_tmap_4d(&tv, p.v, EB, D, p.heads_kv, p.seqlen, p.batch, box, BN, swz)) != FA3B_OK)
     return rc;
   FwdArgs a;
   a.B = p.batch;
@@ -88,7 +89,7 @@ int launch_fwd(const fa3b_fwd_params& p, cudaStream_t stream) {
     a.fp8_thr = 8.f;
     fmt = KIND == KIND_BF16 ? 1u : 0u;
   }
-  const uint32_t idesc_qk = ptx::make_idesc(128, 128, fmt, fmt, false, false, p.alpha < 0);
+  const uint32_t idesc_qk = ptx::make_idesc(128, BN, fmt, fmt, false, false, p.alpha < 0);
   const uint32_t idesc_pv = ptx::make_idesc(128, D, fmt, fmt, false, true, false);
   const int grid = fwd_grid(p.seqlen, NT, p.heads_q, p.batch, CPS);  // persistent CTAs
   kern<<<grid, T::NUM_THREADS, T::SMEM_BYTES, stream>>>(tq, tk, tv, a, idesc_qk, idesc_pv);
@@ -98,11 +99,22 @@ int launch_fwd(const fa3b_fwd_params& p, cudaStream_t stream) {
   return FA3B_OK;
 }
 
-// causal x kind dispatch of one (D, NT, CPS, SCHED, NQ) variant
-template <int D, int NT, int CPS, int SCHED, int KIND, int NQ = 2>
+// causal x kind dispatch of one (D, NT, CPS, SCHED, NQ, BN) variant
+template <int D, int NT, int CPS, int SCHED, int KIND, int NQ = 2, int BN = 128>
 int launch_fwd_c(const fa3b_fwd_params& p, cudaStream_t s) {
-  return p.causal ? launch_fwd<D, NT, true, KIND, CPS, SCHED, NQ>(p, s)
-                  : launch_fwd<D, NT, false, KIND, CPS, SCHED, NQ>(p, s);
+  return p.causal ? launch_fwd<D, NT, true, KIND, CPS, SCHED, NQ, BN>(p, s)
+                  : launch_fwd<D, NT, false, KIND, CPS, SCHED, NQ, BN>(p, s);
+}
+
+// FA3B_FWD_P2=1|0 forces the P2 pair (64-key blocks, one softmax warpgroup per
+// tile, per-tile double S buffers) on or off at d = 128 (A/B switch; the default
+// is the measured choice)
+inline int fwd_p2_env() {
+  static const int v = [] {
+    const char* e = std::getenv("FA3B_FWD_P2");
+    return e == nullptr ? -1 : (std::atoi(e) != 0 ? 1 : 0);
+  }();
+  return v;
 }
 
 // FA3B_FWD_WIDE=1|0 forces the one-tile, four-warpgroup S2 forward (NQ = 4) on or

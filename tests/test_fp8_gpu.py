@@ -305,3 +305,38 @@ def test_prepare_pow2_scales_byte_exact(port, cuda, D, src, hadamard):
         assert np.array_equal(scales[0, h], want_s.astype(np.float32)), h
         assert np.array_equal(codes[0, :, h], want_c), h
         assert np.all(np.log2(scales[0, h]) == np.round(np.log2(scales[0, h])))
+
+
+def test_fp8_p2_pair_variant_matches_default(tmp_path, cuda):
+    """The P2 pair (FA3B_FWD_P2=1: 64-key blocks, one softmax warpgroup per tile,
+    per-tile double S buffers; an A/B alternative, profiles/r02/r02u_p2_pair_ab.log)
+    computes the same FP8 attention as the default ping-pong pair: run in a child
+    process (the switch is read once per process), outputs within FP8 noise."""
+    import subprocess
+    import sys
+    import textwrap
+    import torch
+    from paper_2407_08608_b200 import api
+    script = textwrap.dedent('''
+        import sys, torch
+        sys.path.insert(0, sys.argv[2])
+        from paper_2407_08608_b200 import api
+        g = torch.Generator(device="cuda").manual_seed(11)
+        q, k, v = (torch.randn(2, 1000, 4, 128, device="cuda", generator=g).bfloat16() for _ in range(3))
+        outs = [api.fp8_fwd(q, k, v, causal=c, seed=5, out_dtype=torch.float32) for c in (False, True)]
+        torch.save([(o.cpu(), l.cpu()) for o, l in outs], sys.argv[1])
+    ''')
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parents[1])
+    f = tmp_path / "p2.pt"
+    env = dict(__import__("os").environ, FA3B_FWD_P2="1")
+    subprocess.run([sys.executable, "-c", script, str(f), root], env=env, check=True, timeout=300)
+    p2 = torch.load(f)
+    g = torch.Generator(device="cuda").manual_seed(11)
+    q, k, v = (torch.randn(2, 1000, 4, 128, device="cuda", generator=g).bfloat16() for _ in range(3))
+    for (o2, l2), c in zip(p2, (False, True)):
+        o, l = api.fp8_fwd(q, k, v, causal=c, seed=5, out_dtype=torch.float32)
+        o, l = o.cpu(), l.cpu()
+        assert torch.isfinite(o2).all()
+        assert (o2 - o).norm() <= 0.02 * o.norm(), c
+        assert (l2 - l).abs().max() < 0.02, c
