@@ -179,8 +179,9 @@ struct FwdTraits {
   static constexpr bool P2 = BN == 64;
   static_assert(BN == 128 || (BN == 64 && NT_ == 2 && CPS_ == 1 && SCHED_ == SCHED_DEFAULT && NQ_ == 1),
                 "BN = 64 is the P2 pair");
-  static_assert(NQ == 2 || (NQ == 4 && NT_ == 1 && CPS_ == 1 && SCHED_ != SCHED_NOWS) || (NQ == 1 && P2),
-                "NQ = 4 is one-tile, NQ = 1 the P2 pair");
+  static_assert(NQ == 2 || (NQ == 4 && NT_ == 1 && CPS_ == 1 && SCHED_ != SCHED_NOWS) ||
+                    (NQ == 1 && NT_ == 2 && CPS_ == 1 && SCHED_ == SCHED_DEFAULT),
+                "NQ = 4 is one-tile, NQ = 1 a pair with one warpgroup per tile");
   static constexpr int WPT = 4 * NQ;  // softmax warps per query tile
   static constexpr int EB = EB_;  // bytes per element (2 f16/bf16, 1 e4m3)
   static constexpr int CPS = CPS_;
@@ -1068,8 +1069,11 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
         ptx::tmem_st8(tS + NPK * hh, *reinterpret_cast<uint32_t(*)[8]>(&pk[0]));
       } else if constexpr (NPK == 16) {
         ptx::tmem_st16(tS + NPK * hh, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
-      } else {
+      } else if constexpr (NPK == 32) {
         ptx::tmem_st32(tS + NPK * hh, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+      } else {  // NPK = 64: a whole 128-key row of 16-bit P (NQ = 1)
+        ptx::tmem_st32(tS, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+        ptx::tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
       }
       l = l * factor + psum * (inv_pmul * inv_rho);
       if (tr) FA3B_TP(t, j, 4);

@@ -106,6 +106,16 @@ int launch_fwd_c(const fa3b_fwd_params& p, cudaStream_t s) {
                   : launch_fwd<D, NT, false, KIND, CPS, SCHED, NQ, BN>(p, s);
 }
 
+// FA3B_FWD_Q1=1 runs the d = 128 pair with one softmax warpgroup per query tile
+// (thread = row, all 128 columns: no half-row max exchange) instead of two (A/B switch)
+inline int fwd_q1_env() {
+  static const int v = [] {
+    const char* e = std::getenv("FA3B_FWD_Q1");
+    return e == nullptr ? -1 : (std::atoi(e) != 0 ? 1 : 0);
+  }();
+  return v;
+}
+
 // FA3B_FWD_P2=1|0 forces the P2 pair (64-key blocks, one softmax warpgroup per
 // tile, per-tile double S buffers) on or off at d = 128 (A/B switch; the default
 // is the measured choice)
