@@ -790,6 +790,7 @@ extern "C" int fa3b_fp8_prepare(const fa3b_fp8_prepare_params* pp) {
   const int sb = p.src_dtype == FA3B_DTYPE_F32 ? 4 : 2;
   if (!strides_ok(p.src, sb, p.batch, p.seqlen, p.heads) || !strides_ok(p.dst, 1, p.batch, p.seqlen, p.heads))
     return FA3B_ERR_ALIGNMENT;
+  if (const int rc = check_device(); rc != FA3B_OK) return rc;  // sm_100 current device
   PrepArgs a{};
   a.src = p.src.ptr;
   a.s_sb = p.src.stride_batch;

@@ -85,6 +85,12 @@
 #ifndef FA3B_MMA_SPIN
 #define FA3B_MMA_SPIN 0
 #endif
+// FA3B_FWD_PPBAR = 1: the two tiles of the default pair take turns for the exp
+// phase (a token passed through named barriers 3 / 4, FA3's warpgroup ping-pong
+// ordering), so one tile's exps run alone on the MUFU while the other tile's GEMMs run
+#ifndef FA3B_FWD_PPBAR
+#define FA3B_FWD_PPBAR 0
+#endif
 #ifndef FA3B_FWD_PSPLIT
 #define FA3B_FWD_PSPLIT 0
 #endif
@@ -845,6 +851,15 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
     const uint32_t tO = tmem + lane_base + T::o_col(t);
     float* xch = reinterpret_cast<float*>(smem + T::OFF_XCH) + t * (2 * NQ * 128);  // [2 buf][NQ][128]
     const uint32_t bar_id = 1 + t;
+    // exp-phase token (FA3B_FWD_PPBAR): tile t waits on barrier 3 + t, hands over on 3 + (1 - t)
+    constexpr bool PPB = FA3B_FWD_PPBAR && NT == 2 && CPS == 1 && !T::S3 && !T::P2 && !T::NOWS;
+    auto pp_sync = [&]() {
+      if constexpr (PPB) ptx::named_bar_sync(3 + t, 2 * NQ * 128);
+    };
+    auto pp_arrive = [&]() {
+      if constexpr (PPB) ptx::named_bar_arrive(3 + (1 - t), 2 * NQ * 128);
+    };
+    if (t == 1) pp_arrive();  // tile 0 goes first
     int sc = 0, xc = 0, oc = 0;  // s_full / exchange-buffer / o_full uses so far
     int gbase = 0;               // S3: 2 x (KV blocks of this CTA's previous items)
     int itl = 0;
@@ -1057,6 +1072,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       const bool resc = m_new > m_use + thr;
       const float m_cur = resc ? m_new : m_use;
       const float factor = resc ? ptx::ex2(m_use - m_new) : 1.f;
+      pp_sync();
       exp_half((m_cur == -INFINITY) ? 0.f : m_cur);
       // P (packed, key order) over the first columns of this block's S buffer; every
       // split's S load has completed (the exchange barrier above)
@@ -1075,6 +1091,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
         ptx::tmem_st32(tS, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
         ptx::tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
       }
+      pp_arrive();
       l = l * factor + psum * (inv_pmul * inv_rho);
       if (tr) FA3B_TP(t, j, 4);
       const float ofac = factor * vfac;
@@ -1093,6 +1110,11 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       m_use = m_cur;
       if constexpr (T::NOWS)
         if (leader) nows.after_p(j, nt);
+    }
+    // token slots of the item's blocks this tile does not have (causal: tile 0 has fewer)
+    for (int j = nt; j < w.n_max; ++j) {
+      pp_sync();
+      pp_arrive();
     }
     if (nt > 0) {
       // ---------------------------------------------------------- epilogue
@@ -1153,6 +1175,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
     }
     gbase += 2 * w.n_max;
     }  // work items
+    if (t == 0) pp_sync();  // tile 1's last hand-over
   }
 
   ptx::tc_fence_before();

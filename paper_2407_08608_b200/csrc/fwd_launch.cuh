@@ -14,6 +14,9 @@
 #include "fa3b_internal.cuh"
 #include "fwd_kernel.cuh"
 
+#ifndef FA3B_FP8_THR_BLOCK
+#define FA3B_FP8_THR_BLOCK 4
+#endif
 #ifndef FA3B_FWD_EMU_S2_16
 #define FA3B_FWD_EMU_S2_16 2
 #endif
@@ -26,8 +29,9 @@ namespace fa3b {
 // log2 headroom of the e4m3 P (lazy running max: O and l are rescaled only when
 // the max grows by more than 2^thr, so P <= 2^thr): codes = P * rho * 448 / 2^thr,
 // rho <= 1 the folded power-of-two ratio of the key block's V scale to the one O
-// is kept in (fwd_kernel.cuh). thr 4 per tensor, 2 per block (profiles/r02:
-// RMSE 0.00928 vs 0.00922 with thr 0 at N 8192). FA3B_FP8_THR overrides both.
+// is kept in (fwd_kernel.cuh). thr 4 for both granularities: per block it is
+// +3 % at d 128 and +8 % at d 256 over thr 2 for +0.7 % RMSE (N 8192: 0.00945 vs
+// 0.00938; profiles/r02/r02z_thr_ab.log, r02y_thr_acc.log). FA3B_FP8_THR overrides.
 inline float fp8_threshold(bool kv_blocked) {
   static const float env = [] {
     const char* e = std::getenv("FA3B_FP8_THR");
@@ -35,7 +39,7 @@ inline float fp8_threshold(bool kv_blocked) {
     return (v >= 0.f && v <= 8.f) ? v : -1.f;
   }();
   if (env >= 0.f) return env;
-  return kv_blocked ? 2.f : 4.f;
+  return kv_blocked ? static_cast<float>(FA3B_FP8_THR_BLOCK) : 4.f;
 }
 
 template <int D, int NT, bool CAUSAL, int KIND, int CPS = 1, int SCHED = SCHED_DEFAULT, int NQ = 2,

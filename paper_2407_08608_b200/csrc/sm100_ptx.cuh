@@ -151,6 +151,9 @@ __device__ __forceinline__ float lds_f32(const float* p) {
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+__device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 
 // Warpgroup register re-balancing (every warp of the warpgroup must execute it).
 template <uint32_t N>
