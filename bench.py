@@ -551,12 +551,17 @@ def run_ours(args, rank, world, local_rank):
     achieved = rank_flops / (kernel_ms * 1e-3) / 1e12
     traffic = None
     prof = ROOT / "profiles" / "ncu_summary.json"
-    key = {("c2", False): "fwd_c2_d128", ("c2", True): "fwd_fp8_d128",
-           ("c5", False): "fwd_c5", ("c5", True): "fwd_fp8_c5"}[(args.workload, fp8)]
+    # newest capture of this kernel first (profiles/ncu_summary.json, per launch)
+    keys = {("c2", False): ("fwd_c2_d128_r02", "fwd_c2_d128"),
+            ("c2", True): ("fwd_fp8_d128_r02", "fwd_fp8_d128"),
+            ("c5", False): ("fwd_c5_r02", "fwd_c5"),
+            ("c5", True): ("fwd_fp8_c5_r02", "fwd_fp8_c5")}[(args.workload, fp8)]
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get(key, {}).get("dram_bytes")
-        except (ValueError, OSError):
+            summary = json.loads(prof.read_text())
+            traffic = next((summary[k]["dram_bytes"] for k in keys
+                            if "dram_bytes" in summary.get(k, {})), None)
+        except (ValueError, OSError, KeyError, TypeError):
             traffic = None
     kname = (f"fa3b_fwd_kernel<128,2,{str(causal).lower()},{'e4m3' if fp8 else 'bf16'}>")
     line = {

@@ -88,6 +88,9 @@
 // FA3B_FWD_PPBAR = 1: the two tiles of the default pair take turns for the exp
 // phase (a token passed through named barriers 3 / 4, FA3's warpgroup ping-pong
 // ordering), so one tile's exps run alone on the MUFU while the other tile's GEMMs run
+#ifndef FA3B_FWD_QPREFETCH
+#define FA3B_FWD_QPREFETCH 0
+#endif
 #ifndef FA3B_FWD_PPBAR
 #define FA3B_FWD_PPBAR 0
 #endif
@@ -502,6 +505,21 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       int itl = 0;   // work items so far
       for (int lin = item_of(0); lin < num_items; lin = item_of(++itl)) {
         const Item w = decode(lin);
+        // FA3B_FWD_QPREFETCH: the next item's Q tiles into L2 now, so its TMA load (which
+        // waits for q_empty) finds them there; measured no gain, off
+        // (profiles/r02/r02ad_qprefetch_ab.log)
+#if FA3B_FWD_QPREFETCH
+        if (const int nxt = item_of(itl + 1); nxt < num_items) {
+          const Item wn = decode(nxt);
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            if (wn.n_t[t] == 0) continue;
+#pragma unroll
+            for (int c = 0; c < T::CHUNKS; ++c)
+              ptx::tma_prefetch_4d(&tmQ, c * T::CHUNK_ELEMS, wn.h, wn.q_base + t * 128, wn.b);
+          }
+        }
+#endif
         auto load_q = [&]() {
           if (itl > 0) ptx::mbar_wait(q_empty, (itl - 1) & 1);
           int nvalid = 0;
