@@ -167,17 +167,6 @@ extern "C" {
 
 int fa3b_abi_version(void) { return FA3B_ABI_VERSION; }
 
-#ifdef FA3B_TRACE
-// Debug builds only (-DFA3B_TRACE): copy the forward phase trace to the host.
-__attribute__((visibility("default"))) int fa3b_debug_trace(unsigned long long* out, int n) {
-  const size_t bytes = sizeof(unsigned long long) * static_cast<size_t>(n);
-  return cudaMemcpyFromSymbol(out, fa3b::g_fa3b_trace, bytes) == cudaSuccess ? 0 : -1;
-}
-__attribute__((visibility("default"))) int fa3b_debug_cta_trace(unsigned long long* out, int n) {
-  const size_t bytes = sizeof(unsigned long long) * static_cast<size_t>(n);
-  return cudaMemcpyFromSymbol(out, fa3b::g_fa3b_cta, bytes) == cudaSuccess ? 0 : -1;
-}
-#endif
 int fa3b_last_cuda_error(void) { return g_last_cuda_error; }
 int fa3b_last_launch_count(void) { return g_last_launch_count; }
 

@@ -19,3 +19,21 @@ int launch_fwd16_default_d128(const fa3b_fwd_params& p, cudaStream_t s, bool cta
 }
 
 }  // namespace fa3b
+
+#ifdef FA3B_TRACE
+// Debug builds only (-DFA3B_TRACE): the traces recorded by this translation unit's
+// kernels (the d = 128 f16/bf16 forward): phase points of CTA 0's first item, per-CTA
+// start / end, and CTA 0's item timeline.
+extern "C" __attribute__((visibility("default"))) int fa3b_debug_trace(unsigned long long* out, int n) {
+  const size_t bytes = sizeof(unsigned long long) * static_cast<size_t>(n);
+  return cudaMemcpyFromSymbol(out, fa3b::g_fa3b_trace, bytes) == cudaSuccess ? 0 : -1;
+}
+extern "C" __attribute__((visibility("default"))) int fa3b_debug_cta_trace(unsigned long long* out, int n) {
+  const size_t bytes = sizeof(unsigned long long) * static_cast<size_t>(n);
+  return cudaMemcpyFromSymbol(out, fa3b::g_fa3b_cta, bytes) == cudaSuccess ? 0 : -1;
+}
+extern "C" __attribute__((visibility("default"))) int fa3b_debug_item_trace(unsigned long long* out, int n) {
+  const size_t bytes = sizeof(unsigned long long) * static_cast<size_t>(n);
+  return cudaMemcpyFromSymbol(out, fa3b::g_fa3b_items, bytes) == cudaSuccess ? 0 : -1;
+}
+#endif

