@@ -46,16 +46,20 @@ EncodeTiledFn encode_fn() {
 }
 
 // Ping-pong pairing choice; FA3B_FWD_PAIRING=cta|warp overrides the measured default.
-bool fwd_pairing_impl(int head_dim, bool causal, bool fp8) {
+bool fwd_pairing_impl(int head_dim, bool causal, bool fp8, int seqlen) {
   static const int forced = [] {
     const char* e = std::getenv("FA3B_FWD_PAIRING");
     if (e == nullptr) return -1;
     return std::strcmp(e, "cta") == 0 ? 1 : (std::strcmp(e, "warp") == 0 ? 0 : -1);
   }();
   (void)causal;
-  (void)fp8;
   if (head_dim > 128) return false;
-  return forced == 1;  // warp pairing measured faster on every C2/C3/C5 shape
+  if (forced >= 0) return forced == 1;
+  // Warp pairing (two tiles per CTA) measured faster on every C2/C3/C5 shape at
+  // N 8k (profiles/r01m_pairing_ab.log) and for bf16 at every length; at short
+  // sequences the FP8 forward gains 4-10 % from two one-tile CTAs per SM, whose item
+  // boundaries overlap (profiles/r02/r02af_pairing_short.log)
+  return fp8 && head_dim == 128 && seqlen <= 1024;
 }
 
 }  // namespace
@@ -78,7 +82,9 @@ int check_device() {
   return cache[dev] == 1 ? FA3B_OK : FA3B_ERR_DEVICE;
 }
 
-bool fwd_pairing(int head_dim, bool causal, bool fp8) { return fwd_pairing_impl(head_dim, causal, fp8); }
+bool fwd_pairing(int head_dim, bool causal, bool fp8, int seqlen) {
+  return fwd_pairing_impl(head_dim, causal, fp8, seqlen);
+}
 
 int num_sms() {
   static std::mutex mu;
@@ -244,7 +250,7 @@ int fa3b_fwd(const fa3b_fwd_params* pp) {
   // Ping-pong pairs: two query tiles of one CTA (warp pairing, the default) or
   // one tile in each of two CTAs per SM (CTA pairing, FA3B_FWD_PAIRING=cta);
   // A/B in profiles/r01m_pairing_ab.log.
-  const bool cta_pairs = fwd_pairing(p.head_dim, p.causal != 0, false);
+  const bool cta_pairs = fwd_pairing(p.head_dim, p.causal != 0, false, p.seqlen);
   switch (p.head_dim) {
     case 64: return launch_fwd16_default_d64(p, s, cta_pairs);
     case 128: return launch_fwd16_default_d128(p, s, cta_pairs);

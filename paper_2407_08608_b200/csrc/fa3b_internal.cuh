@@ -45,6 +45,6 @@ inline int fwd_grid(int seqlen, int nt, int heads, int batch, int ctas_per_sm) {
   return static_cast<int>(items < cap ? items : cap);
 }
 // true: pair query tiles across two CTAs per SM; false: two tiles in one CTA
-bool fwd_pairing(int head_dim, bool causal, bool fp8);
+bool fwd_pairing(int head_dim, bool causal, bool fp8, int seqlen);
 
 }  // namespace fa3b

@@ -25,7 +25,7 @@ int launch_fwd_fp8(const fa3b_fwd_params& p, cudaStream_t s) {
       if (fwd_wide_env() == 1) return launch_fwd_c<128, 1, 1, SCHED_DEFAULT, K, 4>(p, s);
       if (fwd_p2_env() == 1) return launch_fwd_c<128, 2, 1, SCHED_DEFAULT, K, 1, 64>(p, s);
       if (fwd_q1_env() == 1) return launch_fwd_c<128, 2, 1, SCHED_DEFAULT, K, 1>(p, s);
-      if (fwd_pairing(128, p.causal != 0, true)) return launch_fwd_c<128, 1, 2, SCHED_DEFAULT, K>(p, s);
+      if (fwd_pairing(128, p.causal != 0, true, p.seqlen)) return launch_fwd_c<128, 1, 2, SCHED_DEFAULT, K>(p, s);
       return launch_fwd_c<128, 2, 1, SCHED_DEFAULT, K>(p, s);
     case 256:
       switch (p.schedule) {
