@@ -57,9 +57,10 @@ bool fwd_pairing_impl(int head_dim, bool causal, bool fp8, int seqlen) {
   if (forced >= 0) return forced == 1;
   // Warp pairing (two tiles per CTA) measured faster on every C2/C3/C5 shape at
   // N 8k (profiles/r01m_pairing_ab.log) and for bf16 at every length; at short
-  // sequences the FP8 forward gains 4-10 % from two one-tile CTAs per SM, whose item
-  // boundaries overlap (profiles/r02/r02af_pairing_short.log)
-  return fp8 && head_dim == 128 && seqlen <= 1024;
+  // sequences (N <= 512) the FP8 forward gains 5-10 % from two one-tile CTAs per SM, whose item
+  // boundaries overlap; at N 1024 it loses 1-3 % (profiles/r02/r02af_pairing_short.log,
+  // r02aj_short.log)
+  return fp8 && head_dim == 128 && seqlen <= 512;
 }
 
 }  // namespace
