@@ -81,7 +81,7 @@ def _fp8_case(port, ref, cuda, N, D, causal, seed, tile=128):
 
 @pytest.mark.parametrize("N,D,causal", [(1024, 128, False), (1024, 128, True), (640, 256, False),
                                         (1000, 256, True), (1024, 64, False), (1000, 64, True),
-                                        (300, 64, False)])
+                                        (300, 64, False), (500, 128, False), (500, 128, True)])
 def test_fp8_fwd_error_band(port, cuda, N, D, causal):
     o, lse, o_ref, l_ref, o_emu, l_emu, *_ = _fp8_case(port, None, cuda, N, D, causal,
                                                         seed=N + D)
