@@ -62,6 +62,8 @@
 // each tile's next S is computed during its own softmax.
 #pragma once
 
+#include <type_traits>
+
 #include "sm100_ptx.cuh"
 
 // Register rebalancing: with FA3B_FWD_REGS = R > 0 the producer / MMA warps get
@@ -90,6 +92,9 @@
 // ordering), so one tile's exps run alone on the MUFU while the other tile's GEMMs run
 #ifndef FA3B_FWD_QB2
 #define FA3B_FWD_QB2 0
+#endif
+#ifndef FA3B_FWD_SPEC
+#define FA3B_FWD_SPEC 0
 #endif
 #ifndef FA3B_FWD_QB2_SHRINK
 #define FA3B_FWD_QB2_SHRINK 0
@@ -209,6 +214,13 @@ struct FwdTraits {
                     (NQ == 1 && NT_ == 2 && CPS_ == 1 && SCHED_ == SCHED_DEFAULT),
                 "NQ = 4 is one-tile, NQ = 1 a pair with one warpgroup per tile");
   static constexpr int WPT = 4 * NQ;  // softmax warps per query tile
+  // P stays in the S columns of the warpgroup that computed it: warpgroup h
+  // owns S columns [h BN/NQ, (h+1) BN/NQ) and writes its P codes to the start of
+  // them, so no warpgroup's P store lands on S another one has yet to read.
+  // PV k-step k (kstep keys = 8 TMEM columns) reads column p_kcol(k).
+  __host__ __device__ static constexpr uint32_t p_kcol(int k, int kstep) {
+    return (k / ((BN / NQ) / kstep)) * (BN / NQ) + (k % ((BN / NQ) / kstep)) * 8;
+  }
   static constexpr int EB = EB_;  // bytes per element (2 f16/bf16, 1 e4m3)
   static constexpr int CPS = CPS_;
   static constexpr int SCHED = SCHED_;
@@ -405,10 +417,10 @@ struct NowsLeader {
       const uint64_t bd = ptx::swz_desc<T::ROW_BYTES>(
           kv_addr + slot * T::KV_TILE_BYTES + k * KSTEP * T::ROW_BYTES, T::KV_CHUNK_BYTES, T::SBO);
       if constexpr (FP8)
-        ptx::mma_f8_ts(tmem + T::o_col(0), tmem + scol + k * 8, bd, idesc_pv,
+        ptx::mma_f8_ts(tmem + T::o_col(0), tmem + scol + T::p_kcol(k, KSTEP), bd, idesc_pv,
                        (j > 0 || k > 0) ? 1u : 0u);
       else
-        ptx::mma_f16_ts(tmem + T::o_col(0), tmem + scol + k * 8, bd, idesc_pv,
+        ptx::mma_f16_ts(tmem + T::o_col(0), tmem + scol + T::p_kcol(k, KSTEP), bd, idesc_pv,
                         (j > 0 || k > 0) ? 1u : 0u);
     }
     ptx::mma_commit(pv_done);
@@ -651,10 +663,10 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
               kv_addr + slot * T::KV_TILE_BYTES + k * KSTEP * T::ROW_BYTES, T::KV_CHUNK_BYTES, T::SBO);
           // A = P in TMEM: KSTEP elements = 8 columns of 32 bits
           if constexpr (FP8)
-            ptx::mma_f8_ts(tmem + T::o_col(t), tmem + scol + k * 8, bd, idesc_pv,
+            ptx::mma_f8_ts(tmem + T::o_col(t), tmem + scol + T::p_kcol(k, KSTEP), bd, idesc_pv,
                            (acc || k > 0) ? 1u : 0u);
           else
-            ptx::mma_f16_ts(tmem + T::o_col(t), tmem + scol + k * 8, bd, idesc_pv,
+            ptx::mma_f16_ts(tmem + T::o_col(t), tmem + scol + T::p_kcol(k, KSTEP), bd, idesc_pv,
                             (acc || k > 0) ? 1u : 0u);
         }
       };
@@ -668,7 +680,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
         for (int k = 0; k < KS; ++k) {
           bd[k] = ptx::swz_desc<T::ROW_BYTES>(kv_addr + slot * T::KV_TILE_BYTES + k * KSTEP * T::ROW_BYTES,
                                               T::KV_CHUNK_BYTES, T::SBO);
-          ta[k] = tmem + scol + k * 8;
+          ta[k] = tmem + scol + T::p_kcol(k, KSTEP);
           asm volatile("" : "+l"(bd[k]), "+r"(ta[k]));
         }
         const uint32_t to = tmem + T::o_col(t);
@@ -1006,7 +1018,10 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
         vs_next = vsp[0];
       }
     }
-    for (int j = 0; j < nt; ++j) {
+    // the block loop body; SPEC (compile time) = exps may start before the max
+    // exchange (blocks j >= 1 with FA3B_FWD_SPEC), block 0 never speculates
+    auto block = [&](const int j, auto spec_c) {
+      constexpr bool SPEC = decltype(spec_c)::value;
       float slj = sl2;
       float vfac = 1.f;  // O rescale for a new V block scale (uniform across the CTA)
       float lrho = 0.f, inv_rho = 1.f;  // FP8: V-scale ratio folded into this block's P
@@ -1130,9 +1145,9 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
           if constexpr (FA3B_FWD_PSPLIT && NPK >= 16) {
             if (i == HC / 4 - 1) {
               if constexpr (NPK == 16)
-                ptx::tmem_st8(tS + NPK * hh, *reinterpret_cast<uint32_t(*)[8]>(&pk[0]));
+                ptx::tmem_st8(tS + HC * hh, *reinterpret_cast<uint32_t(*)[8]>(&pk[0]));
               else
-                ptx::tmem_st16(tS + NPK * hh, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
+                ptx::tmem_st16(tS + HC * hh, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
             }
           }
         }
@@ -1141,6 +1156,13 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       };
       // also: every split's S load of this tile has completed (NQ = 1: a thread's own
       // tcgen05.wait::ld orders its S load before its P store)
+      // FA3B_FWD_SPEC: after the first block the exps start with the running max in
+      // use, before the half-row max exchange completes (P <= 2^thr unless the block
+      // raises the max by more than thr, which is then redone with the new max), so
+      // the exchange barrier overlaps the exps instead of preceding them.
+      // SPEC: the S values die in the speculative exps; a redo (the block raised the
+      // max by more than thr) reloads S from TMEM, which the P store has not touched yet
+      if constexpr (SPEC) exp_half(m_use);
       if constexpr (NQ > 1) ptx::named_bar_sync(bar_id, NQ * 128);
       float mx = pm;
 #pragma unroll
@@ -1151,20 +1173,28 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       const float m_cur = resc ? m_new : m_use;
       const float factor = resc ? ptx::ex2(m_use - m_new) : 1.f;
       pp_sync();
-      exp_half((m_cur == -INFINITY) ? 0.f : m_cur);
+      if constexpr (SPEC) {
+        // tcgen05.ld is warp-collective: the whole warp reloads if any row redoes
+        if (__any_sync(0xffffffffu, resc)) {
+          load_s();
+          if (resc) exp_half(m_cur);
+        }
+      } else {
+        exp_half((m_cur == -INFINITY) ? 0.f : m_cur);
+      }
       // P (packed, key order) over the first columns of this block's S buffer; every
       // split's S load has completed (the exchange barrier above)
       if constexpr (FA3B_FWD_PSPLIT && NPK >= 16) {
         if constexpr (NPK == 16)
-          ptx::tmem_st8(tS + NPK * hh + 8, *reinterpret_cast<uint32_t(*)[8]>(&pk[8]));
+          ptx::tmem_st8(tS + HC * hh + 8, *reinterpret_cast<uint32_t(*)[8]>(&pk[8]));
         else
-          ptx::tmem_st16(tS + NPK * hh + 16, *reinterpret_cast<uint32_t(*)[16]>(&pk[16]));
+          ptx::tmem_st16(tS + HC * hh + 16, *reinterpret_cast<uint32_t(*)[16]>(&pk[16]));
       } else if constexpr (NPK == 8) {
-        ptx::tmem_st8(tS + NPK * hh, *reinterpret_cast<uint32_t(*)[8]>(&pk[0]));
+        ptx::tmem_st8(tS + HC * hh, *reinterpret_cast<uint32_t(*)[8]>(&pk[0]));
       } else if constexpr (NPK == 16) {
-        ptx::tmem_st16(tS + NPK * hh, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
+        ptx::tmem_st16(tS + HC * hh, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
       } else if constexpr (NPK == 32) {
-        ptx::tmem_st32(tS + NPK * hh, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+        ptx::tmem_st32(tS + HC * hh, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
       } else {  // NPK = 64: a whole 128-key row of 16-bit P (NQ = 1)
         ptx::tmem_st32(tS, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
         ptx::tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
@@ -1191,6 +1221,13 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       m_use = m_cur;
       if constexpr (T::NOWS)
         if (leader) nows.after_p(j, nt);
+    };
+    if (nt > 0) block(0, std::false_type{});
+    for (int j = 1; j < nt; ++j) {
+      if constexpr (FA3B_FWD_SPEC)
+        block(j, std::true_type{});
+      else
+        block(j, std::false_type{});
     }
     // token slots of the item's blocks this tile does not have (causal: tile 0 has fewer)
     for (int j = nt; j < w.n_max; ++j) {
