@@ -117,12 +117,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   if (mbar_try_wait(a, parity)) return;
 #if FA3B_WATCHDOG
-  // a suspended try_wait returns at the next barrier event in the CTA, so a wait can
-  // take many rounds: the watchdog reads the clock only every 64th round
+  // (a round counter that reads the clock only every 64th round measured the same
+  // in the forward and costs the d128 backward 256 bytes of spills: -35 %)
   if (mbar_try_wait_sleep(a, parity)) return;
   const long long t0 = clock64();
-  for (uint32_t round = 1; !mbar_try_wait_sleep(a, parity); ++round) {
-    if ((round & 63u) == 0 && clock64() - t0 > (1ll << FA3B_WATCHDOG_LOG2)) {
+  while (!mbar_try_wait_sleep(a, parity)) {
+    if (clock64() - t0 > (1ll << FA3B_WATCHDOG_LOG2)) {
 #ifdef FA3B_WATCHDOG_PRINT
       printf("fa3b watchdog: block %d thread %d smem bar 0x%x parity %u\n", blockIdx.x, threadIdx.x, a, parity);
 #endif
