@@ -13,6 +13,9 @@
 // values (tests/test_fp8_gpu.py). Algorithmic traffic: 2-4 bytes read and 1
 // byte written per element.
 //
+// bf16 input in 128-row blocks (the FP8 forward's case) takes the fast path
+// below: d <= 128 one thread per row (fa3b_fp8_prepare_row_kernel), d = 256 the
+// lane-split kernel over a TMA ring (fa3b_fp8_prepare_fast_kernel). Otherwise:
 // Layout (see Quad): 4 lanes per row at d <= 128 (8 at d = 256), each holding
 // d / 4 (d / 8) contiguous elements, so all but the last two (three) butterfly
 // stages run in registers; vector loads and stores. 128-row blocks at
@@ -452,6 +455,13 @@ struct Fast {
   static constexpr int WARPS = THREADS / 32;
   static constexpr int LOGD = D == 64 ? 6 : (D == 128 ? 7 : 8);
   static constexpr int SPREAD = 23 - LOGD;    // binades an int32 row may span
+  // TMA ring: a 128-row block of bf16 as D / 64 boxes of 128 rows x 128 bytes
+  // (128-byte swizzle), STAGES blocks in flight per CTA
+  static constexpr int CPS = THREADS == 512 ? 2 : 1;  // CTAs per SM
+  static constexpr int STAGES = D == 64 ? 4 : 3;
+  static constexpr int BOX_BYTES = 128 * 128;
+  static constexpr int STAGE_BYTES = 128 * D * 2;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024;  // + alignment slack
 };
 
 __device__ __forceinline__ uint32_t vmax_u16x2(uint32_t a, uint32_t b) {
@@ -522,13 +532,17 @@ __device__ __forceinline__ void fast_row_fp64(const PrepArgs& a, int b, int h, i
   }
 }
 
-// One CTA per 128-row block (grid = blocks x heads x batch); two CTAs per SM at
-// d <= 128 overlap one block's loads with the other's arithmetic. (Measured and
-// not kept: a persistent variant streaming the next block through cp.async, and
-// an L2 prefetch of the next wave's rows; profiles/r02/r02i_prep.log, r02l_prep.log.)
-template <int D, bool HAD>
-__global__ void __launch_bounds__(Fast<D>::THREADS, Fast<D>::THREADS == 512 ? 2 : 1)
-    fa3b_fp8_prepare_fast_kernel(const PrepArgs a) {
+// Persistent CTAs (TMA = true, grid = min(blocks, CPS x SMs)) walk the 128-row
+// blocks c, c + G, ... (blocks of one head are consecutive); the TMA ring keeps
+// the next STAGES - 1 blocks loading while this one is transformed, so the
+// block's barriers no longer leave the SM without loads in flight. TMA = false
+// is the earlier one-CTA-per-block kernel with direct vector loads (grid = blocks;
+// measured and not kept: a persistent variant streaming through cp.async into an
+// unswizzled ring, and an L2 prefetch of the next wave, r02i_prep.log, r02l_prep.log).
+template <int D, bool HAD, bool TMA>
+__global__ void __launch_bounds__(Fast<D>::THREADS, Fast<D>::CPS)
+    fa3b_fp8_prepare_fast_kernel(const __grid_constant__ CUtensorMap tm, const PrepArgs a,
+                                 const int items) {
   using F = Fast<D>;
   constexpr int Q = F::Q, LPR = F::LPR, NP = Q / 2;
   // t32 = RN(I2F(I) * RN(c kLo|Hi)) brackets the exact RN64(RN64(S norm) inv):
@@ -538,11 +552,21 @@ __global__ void __launch_bounds__(Fast<D>::THREADS, Fast<D>::THREADS == 512 ? 2 
   __shared__ double s_red[F::WARPS];
   __shared__ int s_bad[F::WARPS];
   __shared__ double s_bc[2];
+  __shared__ __align__(8) uint64_t s_full[F::STAGES];
+  extern __shared__ uint8_t k5_dyn[];
+  uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(k5_dyn) + 1023) & ~uintptr_t(1023));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, qd = lane % LPR;
-  const int blk = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int row = blk * 128 + warp * F::RPW + lane / LPR;
-  const bool valid = row < a.N;
+  const int rl = warp * F::RPW + lane / LPR;  // row within the block
   const double norm = HAD ? 1.0 / sqrt(static_cast<double>(D)) : 1.0;
+  const int G = static_cast<int>(gridDim.x);
+  auto issue = [&](int stage, int it) {  // one elected thread: block `it` -> ring stage
+    const int hb = it / a.nblk;
+    ptx::mbar_arrive_expect_tx(&s_full[stage], F::STAGE_BYTES);
+#pragma unroll
+    for (int bx = 0; bx < D / 64; ++bx)
+      ptx::tma_load_4d(ring + stage * F::STAGE_BYTES + bx * F::BOX_BYTES, &tm, &s_full[stage], bx * 64,
+                       hb % a.H, (it % a.nblk) * 128, hb / a.H, ptx::kEvictFirst);
+  };
   if constexpr (HAD) {
     for (int i = tid; i < LPR * NP; i += F::THREADS) {
       const int e0 = (i / NP) * Q + 2 * (i % NP), e1 = e0 + 1;
@@ -551,8 +575,35 @@ __global__ void __launch_bounds__(Fast<D>::THREADS, Fast<D>::THREADS == 512 ? 2 
       s_mask[i] = (f0 ? 0x8000u : 0u) | (f1 ? 0x80000000u : 0u);
     }
   }
+  if constexpr (TMA) {
+    if (tid == 0) {
+      ptx::prefetch_tmap(&tm);
+      for (int st = 0; st < F::STAGES; ++st) ptx::mbar_init(&s_full[st], 1);
+      ptx::fence_mbar_init();
+      for (int st = 0; st < F::STAGES; ++st)
+        if (static_cast<int>(blockIdx.x) + st * G < items) issue(st, blockIdx.x + st * G);
+    }
+  }
+  if constexpr (HAD || TMA) __syncthreads();  // s_mask, barrier init
+  int n = 0;
+  for (int it = blockIdx.x; it < items; it += G, ++n) {
+  const int blk = it % a.nblk, h = (it / a.nblk) % a.H, b = it / a.nblk / a.H;
+  const int row = blk * 128 + rl;
+  const bool valid = row < a.N;
   uint32_t w[NP];
-  {
+  if constexpr (TMA) {
+    // rows past N arrive as zeros; chunk c (16 bytes) of row rl sits in box c / 8 at
+    // swizzled position (c % 8) ^ (rl % 8): 4 lanes per bank group, no conflicts
+    const int stage = n % F::STAGES;
+    ptx::mbar_wait(&s_full[stage], (n / F::STAGES) & 1);
+    const uint8_t* sb = ring + stage * F::STAGE_BYTES + rl * 128;
+#pragma unroll
+    for (int k = 0; k < Q / 8; ++k) {
+      const int c = qd * (Q / 8) + k;
+      const uint4 v = *reinterpret_cast<const uint4*>(sb + (c >> 3) * F::BOX_BYTES + (((c & 7) ^ (rl & 7)) << 4));
+      w[4 * k] = v.x; w[4 * k + 1] = v.y; w[4 * k + 2] = v.z; w[4 * k + 3] = v.w;
+    }
+  } else {
     const uint4* src = reinterpret_cast<const uint4*>(
         static_cast<const uint16_t*>(a.src) + b * a.s_sb + static_cast<size_t>(valid ? row : 0) * a.s_ss +
         h * a.s_sh + qd * Q);
@@ -562,7 +613,6 @@ __global__ void __launch_bounds__(Fast<D>::THREADS, Fast<D>::THREADS == 512 ? 2 
       w[4 * k] = v.x; w[4 * k + 1] = v.y; w[4 * k + 2] = v.z; w[4 * k + 3] = v.w;
     }
   }
-  if constexpr (HAD) __syncthreads();  // s_mask
   if constexpr (HAD) {
     const uint4* mk = reinterpret_cast<const uint4*>(s_mask + qd * NP);
 #pragma unroll
@@ -669,8 +719,10 @@ __global__ void __launch_bounds__(Fast<D>::THREADS, Fast<D>::THREADS == 512 ? 2 
     s_red[warp] = v;
     s_bad[warp] = bad;
   }
-  __syncthreads();
+  __syncthreads();  // also: every thread has read this block's ring stage
   if (tid == 0) {
+    if constexpr (TMA)
+      if (it + F::STAGES * G < items) issue(n % F::STAGES, it + F::STAGES * G);
     double m = s_red[0];
     int bd = s_bad[0];
 #pragma unroll
@@ -759,6 +811,282 @@ __global__ void __launch_bounds__(Fast<D>::THREADS, Fast<D>::THREADS == 512 ? 2 
     else
       *reinterpret_cast<uint2*>(drow) = make_uint2(cw[0], cw[1]);
   }
+  }  // blocks of this CTA
+}
+
+// Rare paths of the row kernel kept out of line (one copy instead of one per
+// unrolled group, which would overflow the instruction cache).
+__device__ __noinline__ uint32_t e4m3_group_int(int i0, int i1, int i2, int i3, double pk, double norm,
+                                                double inv) {
+  const int v[4] = {i0, i1, i2, i3};
+  uint32_t code = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) code |= e4m3_sat((static_cast<double>(v[i]) * pk * norm) * inv) << (8 * i);
+  return code;
+}
+__device__ __noinline__ uint32_t e4m3_group_bf16(uint32_t w0, uint32_t w1, double inv) {
+  const float x[4] = {__uint_as_float(w0 << 16), __uint_as_float(w0 & 0xFFFF0000u), __uint_as_float(w1 << 16),
+                      __uint_as_float(w1 & 0xFFFF0000u)};
+  uint32_t code = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) code |= e4m3_sat(static_cast<double>(x[i]) * inv) << (8 * i);
+  return code;
+}
+
+// Row-per-thread variant of the fast path (d <= 128; FA3B_K5_ROW, default on):
+// one CTA of 128 threads per 128-row block, thread r owns row r whole, so the
+// FWHT runs entirely in registers (log2 d stages of IADD pairs, no shuffles), the
+// block's amax barrier spans 4 warps, and 3-4 CTAs per SM overlap one block's
+// TMA load with the others' arithmetic. Same arithmetic as the lane-split kernel
+// above: exact int32 transform, FP32 bracketed encode, FP64 rows and groups.
+template <int D, int LPR>
+struct RowK {
+  static constexpr int LOGD = D == 64 ? 6 : 7;
+  static constexpr int SPREAD = 23 - LOGD;
+  static constexpr int Q = D / LPR;        // elements per thread
+  static constexpr int THREADS = 128 * LPR;
+  static constexpr int WARPS = THREADS / 32;
+  static constexpr int RPW = 32 / LPR;     // rows per warp
+  static constexpr int MINB = Q == 64 ? (LPR == 1 ? 4 : 2) : 3;  // CTAs per SM (registers)
+  static constexpr int BOX_BYTES = 128 * 128;
+  static constexpr int TILE_BYTES = 128 * D * 2;
+  static constexpr int SMEM = TILE_BYTES + 1024;
+};
+
+// One CTA per block (measured: persistent CTAs with a TMA ring of the next tiles
+// were 10-30 % slower than letting the block scheduler refill SMs, r02as_prep.log).
+template <int D, int LPR, bool HAD>
+__global__ void __launch_bounds__(RowK<D, LPR>::THREADS, RowK<D, LPR>::MINB)
+    fa3b_fp8_prepare_row_kernel(const __grid_constant__ CUtensorMap tm, const PrepArgs a) {
+  using R = RowK<D, LPR>;
+  constexpr int Q = R::Q, NP = Q / 2, NC = Q / 8;  // per thread: elements, bf16 pairs, 16-byte chunks
+  constexpr float kLo = 1.f - 8.f / 16777216.f, kHi = 1.f + 8.f / 16777216.f;
+  __shared__ __align__(16) uint32_t s_mask[D / 2];
+  __shared__ double s_red[R::WARPS];
+  __shared__ int s_bad[R::WARPS];
+  __shared__ double s_bc[2];
+  __shared__ __align__(8) uint64_t s_full;
+  extern __shared__ uint8_t k5r_dyn[];
+  uint8_t* tile = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(k5r_dyn) + 1023) & ~uintptr_t(1023));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rl = tid / LPR, part = tid % LPR;  // row within the block, element range of the row
+  const int blk = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int row = blk * 128 + rl;
+  const bool valid = row < a.N;
+  const double norm = HAD ? 1.0 / sqrt(static_cast<double>(D)) : 1.0;
+  if (tid == 0) {
+    ptx::mbar_init(&s_full, 1);
+    ptx::fence_mbar_init();
+    ptx::mbar_arrive_expect_tx(&s_full, R::TILE_BYTES);
+#pragma unroll
+    for (int bx = 0; bx < D / 64; ++bx)
+      ptx::tma_load_4d(tile + bx * R::BOX_BYTES, &tm, &s_full, bx * 64, h, blk * 128, b, ptx::kEvictFirst);
+  }
+  if constexpr (HAD) {
+    for (int i = tid; i < D / 2; i += R::THREADS) {
+      const int e0 = 2 * i, e1 = e0 + 1;
+      const bool f0 = !((a.signs[e0 >> 6] >> (e0 & 63)) & 1ull);
+      const bool f1 = !((a.signs[e1 >> 6] >> (e1 & 63)) & 1ull);
+      s_mask[i] = (f0 ? 0x8000u : 0u) | (f1 ? 0x80000000u : 0u);
+    }
+  }
+  __syncthreads();  // barrier init, s_mask
+  ptx::mbar_wait(&s_full, 0);
+  // chunk c of the row: box c / 8, swizzled slot (c % 8) ^ (row % 8); rows past N are 0
+  const uint8_t* trow = tile + rl * 128;
+  auto chunk = [&](int c) {
+    const int cc = part * NC + c;
+    return *reinterpret_cast<const uint4*>(trow + (cc >> 3) * R::BOX_BYTES + (((cc & 7) ^ (rl & 7)) << 4));
+  };
+  // exponent range of the row (16-bit magnitudes compare like the values)
+  uint32_t mx = 0, mn = 0xFFFFFFFFu;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const uint4 v = chunk(c);
+    const uint32_t q[4] = {v.x & 0x7FFF7FFFu, v.y & 0x7FFF7FFFu, v.z & 0x7FFF7FFFu, v.w & 0x7FFF7FFFu};
+    mx = vmax_u16x2(mx, vmax_u16x2(vmax_u16x2(q[0], q[1]), vmax_u16x2(q[2], q[3])));
+    mn = vmin_u16x2(mn, vmin_u16x2(vmin_u16x2(q[0], q[1]), vmin_u16x2(q[2], q[3])));
+  }
+  uint32_t mx16 = max(mx & 0xFFFFu, mx >> 16), mn16 = min(mn & 0xFFFFu, mn >> 16);
+#pragma unroll
+  for (int o = 1; o < LPR; o <<= 1) {
+    mx16 = max(mx16, __shfl_xor_sync(0xffffffffu, mx16, o));
+    mn16 = min(mn16, __shfl_xor_sync(0xffffffffu, mn16, o));
+  }
+  const int emax = static_cast<int>(mx16 >> 7), emin = static_cast<int>(mn16 >> 7);
+  const bool allzero = mx16 == 0;
+  const int k = 157 - R::LOGD - emax;
+  const bool fast = HAD ? (allzero || (emax <= 254 && emin >= 1 && emin >= emax - R::SPREAD && k <= 127))
+                        : emax <= 254;
+  int I[HAD ? Q : 1];
+  double rowS = 0.0;
+  if constexpr (HAD) {
+    const float fs = (fast && !allzero) ? __uint_as_float(static_cast<uint32_t>(k + 127) << 23) : 0.f;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const uint4 v = chunk(c);
+      const uint4 m = *reinterpret_cast<const uint4*>(s_mask + part * NP + 4 * c);
+      const uint32_t wv[4] = {v.x ^ m.x, v.y ^ m.y, v.z ^ m.z, v.w ^ m.w};
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const float2 x = __fmul2_rn(
+            make_float2(__uint_as_float(wv[p] << 16), __uint_as_float(wv[p] & 0xFFFF0000u)), make_float2(fs, fs));
+        I[8 * c + 2 * p] = __float2int_rn(x.x);
+        I[8 * c + 2 * p + 1] = __float2int_rn(x.y);
+      }
+    }
+#pragma unroll
+    for (int len = 1; len < Q; len <<= 1)
+#pragma unroll
+      for (int e = 0; e < Q; ++e)
+        if ((e & len) == 0) {
+          const int p = I[e], q = I[e + len];
+          I[e] = p + q;
+          I[e + len] = p - q;
+        }
+#pragma unroll
+    for (int m = 1; m < LPR; m <<= 1) {
+      // lower part a + b, upper part a - b = other - mine: one IMAD with sgn = +-1
+      const int sgn = (part & m) ? -1 : 1;
+#pragma unroll
+      for (int e = 0; e < Q; ++e) {
+        const int other = __shfl_xor_sync(0xffffffffu, I[e], m);
+        asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(I[e]) : "r"(I[e]), "r"(sgn), "r"(other));
+      }
+    }
+    int hi_i = I[0], lo_i = I[0];
+#pragma unroll
+    for (int e = 1; e + 1 < Q; e += 2) {
+      hi_i = max(hi_i, max(I[e], I[e + 1]));
+      lo_i = min(lo_i, min(I[e], I[e + 1]));
+    }
+    hi_i = max(hi_i, I[Q - 1]);
+    lo_i = min(lo_i, I[Q - 1]);
+    int rm = max(hi_i, -lo_i);
+#pragma unroll
+    for (int o = 1; o < LPR; o <<= 1) rm = max(rm, __shfl_xor_sync(0xffffffffu, rm, o));
+    rowS = fast ? static_cast<double>(rm) * pow2d(-k) : 0.0;
+  } else {
+    rowS = static_cast<double>(__uint_as_float(mx16 << 16));
+  }
+  // rows outside the fast range: the whole warp, one row at a time, in FP64
+  bool bad = false;
+  const uint32_t slow_rows = __ballot_sync(0xffffffffu, !fast && valid && part == 0);
+  for (uint32_t sr = slow_rows; sr != 0; sr &= sr - 1) {
+    const int src_lane = __ffs(sr) - 1;
+    double sv[D / 32];
+    fast_row_fp64<D, HAD>(a, b, h, blk * 128 + warp * R::RPW + src_lane / LPR, lane, sv);
+    double m = 0.0;
+    bool nf = false;
+#pragma unroll
+    for (int e = 0; e < D / 32; ++e) {
+      nf |= !isfinite(sv[e]);
+      m = fmax(m, fabs(sv[e]));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    nf = __any_sync(0xffffffffu, nf);
+    if (lane / LPR == src_lane / LPR) {
+      rowS = m;
+      bad = nf;
+    }
+  }
+  // block amax, scale = amax / 448, inv = 1 / scale (quantize.cpp:25,55)
+  double v = rowS;
+#pragma unroll
+  for (int o = LPR; o < 32; o <<= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  bad = __any_sync(0xffffffffu, bad);
+  if (lane == 0) {
+    s_red[warp] = v;
+    s_bad[warp] = bad;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double m = s_red[0];
+    int bd = s_bad[0];
+#pragma unroll
+    for (int i = 1; i < R::WARPS; ++i) {
+      m = fmax(m, s_red[i]);
+      bd |= s_bad[i];
+    }
+    const double amax = m * norm;
+    write_scale(a, b, h, blk, amax, bd != 0);
+    const double inv = 1.0 / block_scale(a, amax);
+    s_bc[0] = inv;
+    s_bc[1] = norm * inv;
+  }
+  __syncthreads();
+  const double inv = s_bc[0];
+  uint8_t* dst_row = a.dst + b * a.d_sb + static_cast<size_t>(row) * a.d_ss + h * a.d_sh + part * Q;
+  if (fast && valid) {
+    float c;
+    if constexpr (HAD)
+      c = allzero ? 0.f : static_cast<float>(s_bc[1] * pow2d(-k));
+    else
+      c = inv < 1e38 ? static_cast<float>(inv) : 0.f;
+    const bool huge = !HAD && !(inv < 1e38);
+    const float2 cc = make_float2(c * kLo, c * kHi);
+    // 16 codes (one 16-byte store) at a time
+#pragma unroll
+    for (int s16 = 0; s16 < Q / 16; ++s16) {
+      uint32_t packed[4];
+      uint32_t miss = 0;
+      uint4 raw[2];
+      if constexpr (!HAD) {
+        raw[0] = chunk(2 * s16);
+        raw[1] = chunk(2 * s16 + 1);
+      }
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        float2 t[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          float x;
+          if constexpr (HAD) {
+            x = static_cast<float>(I[16 * s16 + 4 * g + i]);
+          } else {
+            const uint32_t* rw = reinterpret_cast<const uint32_t*>(raw);
+            const uint32_t wp = rw[2 * g + (i >> 1)];
+            x = __uint_as_float((i & 1) ? (wp & 0xFFFF0000u) : (wp << 16));
+          }
+          t[i] = __fmul2_rn(cc, make_float2(x, x));
+        }
+        const uint32_t lo = ptx::pack_e4m3x4(t[0].x, t[1].x, t[2].x, t[3].x);
+        const uint32_t hi = ptx::pack_e4m3x4(t[0].y, t[1].y, t[2].y, t[3].y);
+        packed[g] = lo;
+        miss |= static_cast<uint32_t>(lo != hi) << g;
+      }
+      if (huge) miss = 0xFu;
+      if (miss != 0) {  // rare: the exact FP64 encode for those groups
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          if (!((miss >> g) & 1u)) continue;
+          if constexpr (HAD) {
+            const int* ig = I + 16 * s16 + 4 * g;
+            packed[g] = e4m3_group_int(ig[0], ig[1], ig[2], ig[3], pow2d(-k), norm, inv);
+          } else {
+            const uint32_t* rw = reinterpret_cast<const uint32_t*>(raw);
+            packed[g] = e4m3_group_bf16(rw[2 * g], rw[2 * g + 1], inv);
+          }
+        }
+      }
+      reinterpret_cast<uint4*>(dst_row)[s16] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+    }
+  }
+  for (uint32_t sr = slow_rows; sr != 0; sr &= sr - 1) {
+    const int src_lane = __ffs(sr) - 1;
+    const int r = blk * 128 + warp * R::RPW + src_lane / LPR;
+    double sv[D / 32];
+    fast_row_fp64<D, HAD>(a, b, h, r, lane, sv);
+    uint32_t cw[(D / 32 + 3) / 4] = {};
+#pragma unroll
+    for (int e = 0; e < D / 32; ++e) cw[e >> 2] |= e4m3_sat((sv[e] * norm) * inv) << (8 * (e & 3));
+    uint8_t* drow = a.dst + b * a.d_sb + static_cast<size_t>(r) * a.d_ss + h * a.d_sh + lane * (D / 32);
+    if constexpr (D / 32 == 2)
+      *reinterpret_cast<uint16_t*>(drow) = static_cast<uint16_t>(cw[0]);
+    else
+      *reinterpret_cast<uint32_t*>(drow) = cw[0];
+  }
 }
 
 uint64_t mix64(uint64_t z) {  // rng.cpp:15-19
@@ -821,24 +1149,66 @@ extern "C" int fa3b_fp8_prepare(const fa3b_fp8_prepare_params* pp) {
     return e == nullptr || std::atoi(e) != 0;
   }();
   if (fast_env && p.block_rows == 128 && p.src_dtype == FA3B_DTYPE_BF16 && p.saturate) {
-    auto go = [&](auto kern, int threads) {
-      kern<<<grid, threads, 0, st>>>(a);
+    static const bool tma_env = [] {
+      const char* e = std::getenv("FA3B_K5_TMA");
+      return e == nullptr || std::atoi(e) != 0;
+    }();
+    const int items = a.nblk * p.heads * p.batch;
+    CUtensorMap tm{};
+    if (tma_env) {
+      const int rc = make_tmap_4d(&tm, p.src, 2, p.head_dim, p.heads, p.seqlen, p.batch, 64, 128);
+      if (rc != FA3B_OK) return rc;
+    }
+    auto go = [&](auto tma_kern, auto direct_kern, int threads, int smem, int cps) {
+      if (!tma_env) {
+        direct_kern<<<items, threads, 0, st>>>(tm, a, items);
+        return cudaGetLastError();
+      }
+      const int rc = ensure_smem_attr(reinterpret_cast<const void*>(tma_kern), smem);
+      if (rc != FA3B_OK) return cudaErrorInvalidValue;
+      const int grid = items < cps * num_sms() ? items : cps * num_sms();
+      tma_kern<<<grid, threads, smem, st>>>(tm, a, items);
       return cudaGetLastError();
     };
-    switch (p.head_dim) {
-      case 64:
-        e = p.hadamard ? go(fa3b_fp8_prepare_fast_kernel<64, true>, Fast<64>::THREADS)
-                       : go(fa3b_fp8_prepare_fast_kernel<64, false>, Fast<64>::THREADS);
-        break;
-      case 128:
-        e = p.hadamard ? go(fa3b_fp8_prepare_fast_kernel<128, true>, Fast<128>::THREADS)
-                       : go(fa3b_fp8_prepare_fast_kernel<128, false>, Fast<128>::THREADS);
-        break;
-      default:
-        e = p.hadamard ? go(fa3b_fp8_prepare_fast_kernel<256, true>, Fast<256>::THREADS)
-                       : go(fa3b_fp8_prepare_fast_kernel<256, false>, Fast<256>::THREADS);
-        break;
+#define FA3B_K5_GO(D, HAD) \
+  go(fa3b_fp8_prepare_fast_kernel<D, HAD, true>, fa3b_fp8_prepare_fast_kernel<D, HAD, false>, \
+     Fast<D>::THREADS, Fast<D>::SMEM, Fast<D>::CPS)
+    static const bool row_env = [] {
+      const char* e = std::getenv("FA3B_K5_ROW");
+      return e == nullptr || std::atoi(e) != 0;
+    }();
+    auto go_row = [&](auto kern, int threads, int smem, int mb) {
+      const int rc = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
+      if (rc != FA3B_OK) return cudaErrorInvalidValue;
+      (void)mb;
+      kern<<<grid, threads, smem, st>>>(tm, a);
+      return cudaGetLastError();
+    };
+    if (row_env && p.head_dim <= 128 && !tma_env) {
+      const int rc = make_tmap_4d(&tm, p.src, 2, p.head_dim, p.heads, p.seqlen, p.batch, 64, 128);
+      if (rc != FA3B_OK) return rc;
     }
+    static const int row_lpr = [] {  // lanes per row at d = 128 (A/B: FA3B_K5_LPR=1|2)
+      const char* e = std::getenv("FA3B_K5_LPR");
+      return e != nullptr && std::atoi(e) == 2 ? 2 : 1;
+    }();
+    if (row_env && p.head_dim == 64) {
+      e = p.hadamard ? go_row(fa3b_fp8_prepare_row_kernel<64, 1, true>, RowK<64, 1>::THREADS, RowK<64, 1>::SMEM, RowK<64, 1>::MINB)
+                     : go_row(fa3b_fp8_prepare_row_kernel<64, 1, false>, RowK<64, 1>::THREADS, RowK<64, 1>::SMEM, RowK<64, 1>::MINB);
+    } else if (row_env && p.head_dim == 128 && row_lpr == 1) {
+      e = p.hadamard ? go_row(fa3b_fp8_prepare_row_kernel<128, 1, true>, RowK<128, 1>::THREADS, RowK<128, 1>::SMEM, RowK<128, 1>::MINB)
+                     : go_row(fa3b_fp8_prepare_row_kernel<128, 1, false>, RowK<128, 1>::THREADS, RowK<128, 1>::SMEM, RowK<128, 1>::MINB);
+    } else if (row_env && p.head_dim == 128) {
+      e = p.hadamard ? go_row(fa3b_fp8_prepare_row_kernel<128, 2, true>, RowK<128, 2>::THREADS, RowK<128, 2>::SMEM, RowK<128, 2>::MINB)
+                     : go_row(fa3b_fp8_prepare_row_kernel<128, 2, false>, RowK<128, 2>::THREADS, RowK<128, 2>::SMEM, RowK<128, 2>::MINB);
+    } else {
+      switch (p.head_dim) {
+        case 64: e = p.hadamard ? FA3B_K5_GO(64, true) : FA3B_K5_GO(64, false); break;
+        case 128: e = p.hadamard ? FA3B_K5_GO(128, true) : FA3B_K5_GO(128, false); break;
+        default: e = p.hadamard ? FA3B_K5_GO(256, true) : FA3B_K5_GO(256, false); break;
+      }
+    }
+#undef FA3B_K5_GO
     if (e != cudaSuccess) return cuda_fail(e);
   } else if (p.block_rows == 128 && p.head_dim <= 128) {
     // d = 256 would hold 64 doubles per thread; it takes the two-pass kernel instead

@@ -257,6 +257,28 @@ def test_prepare_bf16_fast_path_full_size(port, cuda):
             assert np.array_equal(scales[0, h].cpu().numpy(), want_s.astype(np.float32)), (had, h)
 
 
+@pytest.mark.parametrize("D", [64, 128, 256])
+def test_prepare_bf16_fast_path_persistent_strided(port, cuda, D):
+    # persistent CTAs walk several blocks each through the TMA ring (2 x 33 blocks x
+    # H heads > CTAs), the last block ragged (N = 4100), the input a strided view of
+    # a packed [B, N, 3, H, d] qkv tensor: sampled (batch, head) pairs byte-exact
+    from paper_2407_08608_b200 import api
+    import torch
+    B, N, H = 2, 4100, 2048 // D
+    g = torch.Generator(device="cuda").manual_seed(D)
+    qkv = torch.randn(B, N, 3, H, D, device="cuda", generator=g, dtype=torch.bfloat16)
+    x = qkv[:, :, 1]
+    for had in (True, False):
+        codes, scales = api.fp8_prepare(x, block_rows=128, hadamard=had, seed=9)
+        for b, h in ((0, 0), (0, H - 1), (1, H // 2), (1, H - 1)):
+            m = x[b, :, h].double().cpu().numpy()
+            if had:
+                m, _ = port.preprocess_incoherent(m, m, 9)
+            want_c, want_s = port.quantize(m, 128)
+            assert np.array_equal(codes[b, :, h].float().cpu().numpy(), want_c), (had, b, h)
+            assert np.array_equal(scales[b, h].cpu().numpy(), want_s.astype(np.float32)), (had, b, h)
+
+
 def test_prepare_bf16_nonfinite_block_reports_nan_scale(cuda):
     # the reference throws on non-finite input (quantize.cpp:15); the device marks
     # the block's scale NaN and leaves the other blocks intact
