@@ -96,6 +96,10 @@
 #ifndef FA3B_FWD_SPEC
 #define FA3B_FWD_SPEC 0
 #endif
+// release Q after the item's last S (not after its last PV): see the MMA warp
+#ifndef FA3B_FWD_QEARLY
+#define FA3B_FWD_QEARLY 1
+#endif
 #ifndef FA3B_FWD_QB2_SHRINK
 #define FA3B_FWD_QB2_SHRINK 0
 #endif
@@ -891,6 +895,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
           }
           FA3B_IT(itl, 10);
           ptx::mma_commit(&kv_empty[slot0]);
+          if (FA3B_FWD_QEARLY && w.n_max == 1) ptx::mma_commit(qe(itl));  // every S issued
         }
         for (int j = 0; j < w.n_max; ++j) {
           const int item_v = kvi + 2 * j + 1, item_k = kvi + 2 * j + 2;
@@ -923,8 +928,11 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
           }
           ptx::mma_commit(&kv_empty[slot_v]);
           if (k_ready) ptx::mma_commit(&kv_empty[slot_k]);
+          // QEARLY: Q is released once the item's last S MMAs complete, so the next
+          // item's Q load overlaps this item's last softmax, PVs and epilogue
+          if (FA3B_FWD_QEARLY && j + 2 == w.n_max) ptx::mma_commit(qe(itl));
         }
-        ptx::mma_commit(qe(itl));  // fires once every MMA of this item has read Q
+        if (!FA3B_FWD_QEARLY) ptx::mma_commit(qe(itl));  // once every MMA of this item has read Q
         kvi += 2 * w.n_max;
       }
     }
