@@ -171,6 +171,7 @@ struct FwdArgs {
   void* o;
   long long o_sb, o_ss, o_sh;  // element strides of O
   int out_f32;
+  int o_v8;           // 16-bit O rows 32-byte aligned: 256-bit stores in the epilogue
   float* lse;         // [B, H, N] or nullptr
   // E4M3 only
   const float* q_scale;  // [B, H, nqb] (per 128-row block) or [B, H] (per tensor)
@@ -1288,10 +1289,18 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
             const float bb = __uint_as_float(ov[2 * i + 1]) * inv;
             pk[i] = (BF16 || FP8) ? ptx::pack_bf16(a, bb) : ptx::pack_f16(a, bb);
           }
-          uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(args.o) + obase + c * CW);
+          uint16_t* orow = static_cast<uint16_t*>(args.o) + obase + c * CW;
+          if (CW % 16 == 0 && args.o_v8) {
+            // one sector per lane and instruction (STG.256): half the store wavefronts
 #pragma unroll
-          for (int i = 0; i < CW / 8; ++i)
-            dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+            for (int i = 0; i < CW / 16; ++i)
+              ptx::st_global_v8(orow + 16 * i, &pk[8 * i]);
+          } else {
+            uint4* dst = reinterpret_cast<uint4*>(orow);
+#pragma unroll
+            for (int i = 0; i < CW / 8; ++i)
+              dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+          }
         }
       }
       if (hh == 0 && row_ok && args.lse != nullptr) {

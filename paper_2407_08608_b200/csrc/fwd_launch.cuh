@@ -75,6 +75,12 @@ int launch_fwd(const fa3b_fwd_params& p, cudaStream_t stream) {
   a.o_ss = p.o.stride_seq;
   a.o_sh = p.o.stride_head;
   a.out_f32 = p.out_dtype == FA3B_DTYPE_F32;
+  {
+    // 32-byte aligned 16-bit rows: base and every stride a multiple of 16 elements
+    auto ok32 = [](long long st, int extent) { return extent <= 1 || st % 16 == 0; };
+    a.o_v8 = !a.out_f32 && (reinterpret_cast<uintptr_t>(p.o.ptr) & 31u) == 0 && ok32(a.o_sb, p.batch) &&
+             ok32(a.o_ss, p.seqlen) && ok32(a.o_sh, p.heads_q);
+  }
   a.lse = p.lse;
   uint32_t fmt = 0;
   if constexpr (FP8) {
