@@ -127,6 +127,7 @@ struct BwdArgs {
   long long dk_sb, dk_ss, dk_sh;
   void* dv;
   long long dv_sb, dv_ss, dv_sh;
+  int dkv_v8;  // dK and dV rows 32-byte aligned: 256-bit stores
 };
 
 // K3 layout. Warps 0-7: two gradient warpgroups (warpgroup w owns query columns
@@ -249,7 +250,8 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
   const int N = args.N;
   const int nq = args.Npad / 128;
   const int HB = args.Hkv * args.B;
-  const int num_items = nq * HB;
+  // recomputed from the kernel parameters at each use (a register-resident copy spills)
+#define num_items ((args.Npad / 128) * args.Hkv * args.B)
   auto item_of = [&](int k) {
     const int G = static_cast<int>(gridDim.x), c = static_cast<int>(blockIdx.x);
     return k * G + ((CAUSAL && (k & 1)) ? G - 1 - c : c);
@@ -694,9 +696,15 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
           const float a0 = __uint_as_float(v[2 * e]) * scale, a1 = __uint_as_float(v[2 * e + 1]) * scale;
           pk2[e] = BF16 ? ptx::pack_bf16(a0, a1) : ptx::pack_f16(a0, a1);
         }
-        uint4* dst = reinterpret_cast<uint4*>(base + off + w * (D / 2) + c * 32);
+        uint16_t* orow = base + off + w * (D / 2) + c * 32;
+        if (args.dkv_v8) {
+          ptx::st_global_v8(orow, &pk2[0]);
+          ptx::st_global_v8(orow + 16, &pk2[8]);
+        } else {
+          uint4* dst = reinterpret_cast<uint4*>(orow);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) dst[e] = make_uint4(pk2[4 * e], pk2[4 * e + 1], pk2[4 * e + 2], pk2[4 * e + 3]);
+          for (int e = 0; e < 4; ++e) dst[e] = make_uint4(pk2[4 * e], pk2[4 * e + 1], pk2[4 * e + 2], pk2[4 * e + 3]);
+        }
       }
     }
     }  // work items
@@ -709,6 +717,7 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
     ptx::tmem_dealloc<512>(tmem);
   }
 }
+#undef num_items
 
 size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
@@ -774,6 +783,14 @@ int launch_bwd_main(const fa3b_bwd_params& p, const Workspace& ws, int Npad, cud
   a.dv_sb = p.dv.stride_batch;
   a.dv_ss = p.dv.stride_seq;
   a.dv_sh = p.dv.stride_head;
+  {
+    auto ok32 = [&](const fa3b_tensor4& t) {
+      auto st = [](long long x, int extent) { return extent <= 1 || x % 16 == 0; };
+      return (reinterpret_cast<uintptr_t>(t.ptr) & 31u) == 0 && st(t.stride_batch, p.batch) &&
+             st(t.stride_seq, p.seqlen) && st(t.stride_head, p.heads_kv);
+    };
+    a.dkv_v8 = ok32(p.dk) && ok32(p.dv);
+  }
   const uint32_t fmt = BF16 ? 1u : 0u;
   const uint32_t idesc_s = ptx::make_idesc(128, 128, fmt, fmt, false, false, p.alpha < 0);
   const uint32_t idesc_dp = ptx::make_idesc(128, 128, fmt, fmt, false, false, false);
