@@ -841,13 +841,13 @@ __device__ __noinline__ uint32_t e4m3_group_bf16(uint32_t w0, uint32_t w1, doubl
 // above: exact int32 transform, FP32 bracketed encode, FP64 rows and groups.
 template <int D, int LPR>
 struct RowK {
-  static constexpr int LOGD = D == 64 ? 6 : 7;
+  static constexpr int LOGD = D == 64 ? 6 : (D == 128 ? 7 : 8);
   static constexpr int SPREAD = 23 - LOGD;
   static constexpr int Q = D / LPR;        // elements per thread
   static constexpr int THREADS = 128 * LPR;
   static constexpr int WARPS = THREADS / 32;
   static constexpr int RPW = 32 / LPR;     // rows per warp
-  static constexpr int MINB = Q == 64 ? (LPR == 1 ? 4 : 2) : 3;  // CTAs per SM (registers)
+  static constexpr int MINB = THREADS == 512 ? 1 : (Q == 64 ? (LPR == 1 ? 4 : 2) : (THREADS == 256 ? 1 : 3));  // CTAs per SM (registers)
   static constexpr int BOX_BYTES = 128 * 128;
   static constexpr int TILE_BYTES = 128 * D * 2;
   static constexpr int SMEM = TILE_BYTES + 1024;
@@ -1084,8 +1084,10 @@ __global__ void __launch_bounds__(RowK<D, LPR>::THREADS, RowK<D, LPR>::MINB)
     uint8_t* drow = a.dst + b * a.d_sb + static_cast<size_t>(r) * a.d_ss + h * a.d_sh + lane * (D / 32);
     if constexpr (D / 32 == 2)
       *reinterpret_cast<uint16_t*>(drow) = static_cast<uint16_t>(cw[0]);
-    else
+    else if constexpr (D / 32 == 4)
       *reinterpret_cast<uint32_t*>(drow) = cw[0];
+    else
+      *reinterpret_cast<uint2*>(drow) = make_uint2(cw[0], cw[1]);
   }
 }
 
@@ -1184,13 +1186,17 @@ extern "C" int fa3b_fp8_prepare(const fa3b_fp8_prepare_params* pp) {
       kern<<<grid, threads, smem, st>>>(tm, a);
       return cudaGetLastError();
     };
-    if (row_env && p.head_dim <= 128 && !tma_env) {
+    if (row_env && !tma_env) {
       const int rc = make_tmap_4d(&tm, p.src, 2, p.head_dim, p.heads, p.seqlen, p.batch, 64, 128);
       if (rc != FA3B_OK) return rc;
     }
     static const int row_lpr = [] {  // lanes per row at d = 128 (A/B: FA3B_K5_LPR=1|2)
       const char* e = std::getenv("FA3B_K5_LPR");
       return e != nullptr && std::atoi(e) == 2 ? 2 : 1;
+    }();
+    static const int row_lpr256 = [] {  // d = 256: 0 = lane-split TMA-ring kernel, else lanes per row
+      const char* e = std::getenv("FA3B_K5_LPR256");
+      return e != nullptr ? std::atoi(e) : 2;
     }();
     if (row_env && p.head_dim == 64) {
       e = p.hadamard ? go_row(fa3b_fp8_prepare_row_kernel<64, 1, true>, RowK<64, 1>::THREADS, RowK<64, 1>::SMEM, RowK<64, 1>::MINB)
@@ -1201,6 +1207,12 @@ extern "C" int fa3b_fp8_prepare(const fa3b_fp8_prepare_params* pp) {
     } else if (row_env && p.head_dim == 128) {
       e = p.hadamard ? go_row(fa3b_fp8_prepare_row_kernel<128, 2, true>, RowK<128, 2>::THREADS, RowK<128, 2>::SMEM, RowK<128, 2>::MINB)
                      : go_row(fa3b_fp8_prepare_row_kernel<128, 2, false>, RowK<128, 2>::THREADS, RowK<128, 2>::SMEM, RowK<128, 2>::MINB);
+    } else if (row_env && p.head_dim == 256 && row_lpr256 == 2) {
+      e = p.hadamard ? go_row(fa3b_fp8_prepare_row_kernel<256, 2, true>, RowK<256, 2>::THREADS, RowK<256, 2>::SMEM, RowK<256, 2>::MINB)
+                     : go_row(fa3b_fp8_prepare_row_kernel<256, 2, false>, RowK<256, 2>::THREADS, RowK<256, 2>::SMEM, RowK<256, 2>::MINB);
+    } else if (row_env && p.head_dim == 256 && row_lpr256 == 4) {
+      e = p.hadamard ? go_row(fa3b_fp8_prepare_row_kernel<256, 4, true>, RowK<256, 4>::THREADS, RowK<256, 4>::SMEM, RowK<256, 4>::MINB)
+                     : go_row(fa3b_fp8_prepare_row_kernel<256, 4, false>, RowK<256, 4>::THREADS, RowK<256, 4>::SMEM, RowK<256, 4>::MINB);
     } else {
       switch (p.head_dim) {
         case 64: e = p.hadamard ? FA3B_K5_GO(64, true) : FA3B_K5_GO(64, false); break;
