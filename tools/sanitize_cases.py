@@ -1,7 +1,7 @@
 """Small shapes of every kernel for compute-sanitizer (tools/sanitize.sh):
 K1 (bf16 fwd d64/128/256, causal and ragged, schedule variants), K2-K4 (bwd d64/128,
-both dQ modes), K5 (FP64 and bf16 fast paths, per block and per tensor), K6 (e4m3
-fwd d128/256)."""
+both dQ modes), K5 (FP64 and bf16 fast paths incl. the row kernels, per block and per tensor),
+K6 (e4m3 fwd d64/128/256)."""
 import sys
 import torch
 sys.path.insert(0, ".")
@@ -21,7 +21,7 @@ for d in (64, 128, 256):
             for blk in (128, 0):
                 api.fp8_prepare(q, block_rows=blk, hadamard=had, seed=1)
                 api.fp8_prepare(q.float(), block_rows=blk, hadamard=had, seed=1)
-        if d >= 128:
+        if True:  # FP8 forward at every head dim (d 64: 64-byte swizzled tiles)
             api.fp8_fwd(q, k, v, causal=causal, seed=3)
             api.fp8_fwd(q, k, v, causal=causal, seed=3, per_block=False)
 q, k, v = (torch.randn(1, 256, 2, 128, device=dev, dtype=torch.float16) for _ in range(3))
