@@ -189,7 +189,7 @@ __device__ __forceinline__ void quad_store(const PrepArgs& a, int b, int h, int 
         if (static_cast<double>(z) != t) z = __uint_as_float(__float_as_uint(z) | 1u);
         f[u] = z;
       }
-      packed[e >> 2] = ptx::pack_e4m3x4(f[0], f[1], f[2], f[3]);
+      packed[e >> 2] = ptx::pack_e4m3x4_merge(f[0], f[1], f[2], f[3]);
     }
   } else {
 #pragma unroll
@@ -482,7 +482,7 @@ __device__ __forceinline__ double pow2d(int e) {  // 2^e, |e| <= 1022
 __device__ __forceinline__ uint32_t e4m3_sat(double t) {
   float z = __double2float_rz(t);
   if (static_cast<double>(z) != t) z = __uint_as_float(__float_as_uint(z) | 1u);
-  return ptx::pack_e4m3x4(z, 0.f, 0.f, 0.f) & 0xFFu;
+  return ptx::pack_e4m3x4_merge(z, 0.f, 0.f, 0.f) & 0xFFu;
 }
 
 // One row by the whole warp in FP64 (lane l holds entries [l M, l M + M)), the
@@ -765,8 +765,8 @@ __global__ void __launch_bounds__(Fast<D>::THREADS, Fast<D>::CPS)
         }
         t[i] = __fmul2_rn(cc, make_float2(x, x));
       }
-      const uint32_t lo = ptx::pack_e4m3x4(t[0].x, t[1].x, t[2].x, t[3].x);
-      const uint32_t hi = ptx::pack_e4m3x4(t[0].y, t[1].y, t[2].y, t[3].y);
+      const uint32_t lo = ptx::pack_e4m3x4_merge(t[0].x, t[1].x, t[2].x, t[3].x);
+      const uint32_t hi = ptx::pack_e4m3x4_merge(t[0].y, t[1].y, t[2].y, t[3].y);
       packed[g] = lo;
       miss |= static_cast<uint32_t>(lo != hi) << g;
     }
@@ -1051,8 +1051,8 @@ __global__ void __launch_bounds__(RowK<D, LPR>::THREADS, RowK<D, LPR>::MINB)
           }
           t[i] = __fmul2_rn(cc, make_float2(x, x));
         }
-        const uint32_t lo = ptx::pack_e4m3x4(t[0].x, t[1].x, t[2].x, t[3].x);
-        const uint32_t hi = ptx::pack_e4m3x4(t[0].y, t[1].y, t[2].y, t[3].y);
+        const uint32_t lo = ptx::pack_e4m3x4_merge(t[0].x, t[1].x, t[2].x, t[3].x);
+        const uint32_t hi = ptx::pack_e4m3x4_merge(t[0].y, t[1].y, t[2].y, t[3].y);
         packed[g] = lo;
         miss |= static_cast<uint32_t>(lo != hi) << g;
       }
