@@ -193,6 +193,31 @@ def test_strided_inputs(port, cuda):
     assert torch.equal(o1, o2) and torch.equal(l1, l2)
 
 
+@pytest.mark.parametrize("D", [64, 128, 256])
+def test_output_rows_16_byte_aligned(cuda, D):
+    """O (and dK / dV) rows only 16-byte aligned (head stride D + 8 elements): the
+    epilogues fall back from 256-bit to 128-bit stores; results bitwise equal to
+    the contiguous, 32-byte aligned outputs."""
+    api = _api()
+    torch = _torch()
+    B, N, H = 2, 300, 2
+    g = torch.Generator(device="cuda").manual_seed(D)
+    q, k, v, do = (torch.randn(B, N, H, D, device="cuda", generator=g, dtype=torch.bfloat16)
+                   for _ in range(4))
+    o1, l1 = api.fwd(q, k, v, causal=True)
+    wide = torch.zeros(B, N, H, D + 8, device="cuda", dtype=torch.bfloat16)
+    o2, l2 = api.fwd(q, k, v, causal=True, out=wide[..., :D])
+    assert o2.data_ptr() == wide.data_ptr() and torch.equal(o1, o2) and torch.equal(l1, l2)
+    assert torch.count_nonzero(wide[..., D:]) == 0  # nothing written past the view
+    if D <= 128:
+        g1 = api.bwd(q, k, v, o1, do, l1, causal=True, deterministic=True)
+        dkw, dvw = (torch.zeros(B, N, H, D + 8, device="cuda", dtype=torch.bfloat16) for _ in range(2))
+        g2 = api.bwd(q, k, v, o1, do, l1, causal=True, deterministic=True, dk=dkw[..., :D], dv=dvw[..., :D])
+        for a, b_ in zip(g1, g2):
+            assert torch.equal(a, b_)
+        assert torch.count_nonzero(dkw[..., D:]) == 0 and torch.count_nonzero(dvw[..., D:]) == 0
+
+
 @pytest.mark.parametrize("D,causal", [(128, False), (128, True), (64, True), (256, False)])
 def test_full_size_against_torch_rows(cuda, D, causal):
     """C2 at N = 16k (B = 1, H = 2048 / D): a sample of query rows checked
