@@ -16,3 +16,11 @@ int launch_fwd16_default_d64(const fa3b_fwd_params& p, cudaStream_t s, bool cta_
 }
 
 }  // namespace fa3b
+
+#ifdef FA3B_TRACE
+// Debug builds only (-DFA3B_TRACE): the phase points recorded by the d = 64 forward.
+extern "C" __attribute__((visibility("default"))) int fa3b_debug_trace_d64(unsigned long long* out, int n) {
+  const size_t bytes = sizeof(unsigned long long) * static_cast<size_t>(n);
+  return cudaMemcpyFromSymbol(out, fa3b::g_fa3b_trace, bytes) == cudaSuccess ? 0 : -1;
+}
+#endif
