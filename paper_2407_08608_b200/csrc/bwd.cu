@@ -191,6 +191,9 @@ struct BwdTraits {
 #ifndef FA3B_BWD_EMU128
 #define FA3B_BWD_EMU128 0
 #endif
+#ifndef FA3B_BWD_KVPREFETCH
+#define FA3B_BWD_KVPREFETCH 0
+#endif
 #ifndef FA3B_BWD_S_EARLY
 #define FA3B_BWD_S_EARLY 1
 #endif
@@ -336,6 +339,18 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
             ptx::tma_load_4d(smem + T::OFF_V + c * T::CHUNK_BYTES, &tmV, kv_full, c * 64, w.hkv, w.j * 128,
                              w.b, ptx::kEvictFirst);
           }
+#if FA3B_BWD_KVPREFETCH
+          // the next item's K / V into L2 now (its TMA load waits for kv_empty, this
+          // item's last MMAs): measured 3-7 % slower at d 64 N <= 1k, neutral at d 128
+          // (profiles/r02/r02bc_kvpf_ab.log), off
+          if (const int nxt = item_of(itl + 1); nxt < num_items) {
+            const Item wn = decode(nxt);
+            for (int c = 0; c < D / 64; ++c) {
+              ptx::tma_prefetch_4d(&tmK, c * 64, wn.hkv, wn.j * 128, wn.b);
+              ptx::tma_prefetch_4d(&tmV, c * 64, wn.hkv, wn.j * 128, wn.b);
+            }
+          }
+#endif
           for (int it = 0; it < w.n_iter; ++it, ++gi) {
             const int h = w.hkv * args.group + it / w.per_head;
             const int i = w.i0 + it % w.per_head;

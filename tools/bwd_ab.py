@@ -1,5 +1,5 @@
 """Interleaved A/B of the backward (K2 + K3 + K4) across libfa3b.so builds, like
-tools/ab.py: C4 shapes at N 8192. Usage: python tools/bwd_ab.py lib1.so lib2.so ..."""
+tools/ab.py: C4 shapes at N 8192 (BWD_N=512,1024,... for others). Usage: python tools/bwd_ab.py lib1.so lib2.so ..."""
 import os
 import sys
 
@@ -27,15 +27,17 @@ def timeit(f, it=5):
 
 
 cases = []
-for D, causal, det in ((128, False, False), (128, True, False), (64, False, False), (128, False, True)):
-    N, B, H = 8192, 2, 2048 // D
+NS = [int(x) for x in os.environ.get("BWD_N", "8192").split(",")]  # C4 lengths (B = 16384 / N)
+for N, D, causal, det in [(n, *c) for n in NS for c in ((128, False, False), (128, True, False), (64, False, False),
+                                                       (128, False, True))]:
+    B, H = 16384 // N, 2048 // D
     q, k, v, do = (torch.randn(B, N, H, D, device="cuda", dtype=torch.bfloat16) for _ in range(4))
     _lib._lib = libs[0]
     o, lse = api.fwd(q, k, v, causal=causal)
     ws = torch.empty(api.bwd_workspace_bytes(B, H, H, N, D), dtype=torch.uint8, device="cuda")
     g = [torch.empty_like(q) for _ in range(3)]
     fl = 2.5 * 4 * N * N * D * H * B / (2 if causal else 1)
-    cases.append((f"bwd d{D}{'c' if causal else ''}{'det' if det else ''}", fl,
+    cases.append((f"N{N} d{D}{'c' if causal else ''}{'det' if det else ''}", fl,
                   (lambda q=q, k=k, v=v, o=o, do=do, lse=lse, c=causal, ws=ws, g=g, det=det:
                    api.bwd(q, k, v, o, do, lse, causal=c, dq=g[0], dk=g[1], dv=g[2], workspace=ws,
                            deterministic=det))))
