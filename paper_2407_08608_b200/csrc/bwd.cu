@@ -43,7 +43,18 @@ __device__ unsigned long long g_fa3b_bwd_trace[64][16];
     if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (it) < 64)               \
       g_fa3b_bwd_trace[it][k] = clock64();                                                 \
   } while (0)
+// per-item timeline of CTA 0 (items < 32): [0] producer issues K/V, [1] MMA sees
+// K/V, [2] MMA issues the first S, [3] MMA issues the item's last dQ, [4] epilogue
+// starts (dK/dV ready), [5] epilogue done; read with fa3b_debug_bwd_items()
+__device__ unsigned long long g_fa3b_bwd_items[32][8];
+#define BWD_IT(itl, k)                                                                     \
+  do {                                                                                     \
+    if (blockIdx.x == 0 && (itl) < 32) g_fa3b_bwd_items[itl][k] = clock64();               \
+  } while (0)
 #else
+#define BWD_IT(itl, k) \
+  do {                 \
+  } while (0)
 #define BWD_TP(it, k) \
   do {                \
   } while (0)
@@ -156,6 +167,9 @@ struct BwdArgs {
 //   dV += P_i^T dO_i | dK += dS_i^T Q_i | S_{i+1} = K Q_{i+1}^T | dQ_i | dP_{i+1} = V dO_{i+1}^T
 // with the softmax split in two phases (P_i after S_i lands, dS_i after dP_i), so
 // dV_i starts while dS_i is still being formed and S_{i+1} runs under dQ_i.
+#ifndef FA3B_BWD_KV2
+#define FA3B_BWD_KV2 0
+#endif
 template <int D_>
 struct BwdTraits {
   static constexpr int D = D_;
@@ -172,16 +186,22 @@ struct BwdTraits {
   static constexpr int LOAD_WARP = 12;
   static constexpr int MMA_WARP = 13;
   static constexpr int NUM_THREADS = 16 * 32;
+  // KVB K/V buffers: with two (FA3B_BWD_KV2, d = 64, where shared memory allows)
+  // the next work item's K and V load during this item instead of after its last
+  // MMA. Measured no gain at N 512-8k (r02be_kv2_ab.log): the item boundary is
+  // the gradient warps' dK / dV epilogue (bwd item trace r02bd), not the load. Off.
+  static constexpr int KVB = (D == 64 && FA3B_BWD_KV2) ? 2 : 1;
   static constexpr int OFF_K = 0;
   static constexpr int OFF_V = TILE_BYTES;
-  static constexpr int OFF_RING = 2 * TILE_BYTES;
+  static constexpr int KV_STRIDE = 2 * TILE_BYTES;  // buffer b at + b KV_STRIDE
+  static constexpr int OFF_RING = KVB * 2 * TILE_BYTES;
   static constexpr int OFF_DS = OFF_RING + RING * TILE_BYTES;  // 128 kv x 128 q 16-bit
   static constexpr int OFF_STG = OFF_DS + 2 * CHUNK_BYTES;      // dQ boxes 2 x (128 x 32 fp32)
   static constexpr int OFF_VEC = OFF_STG + 2 * CHUNK_BYTES;     // LSE2[2][128], Delta[2][128]
   static constexpr int OFF_BAR = OFF_VEC + 4 * 512;
   // kv_full, ring_full[RING], ring_empty[RING], vec_full[2], vec_empty[2], s_full,
   // dp_full, pa_full, pb_full, dq_full, dq_free, dkv_full, kv_empty
-  static constexpr int NUM_BARS = 13 + 2 * RING;
+  static constexpr int NUM_BARS = 13 + 2 * RING + 2 * (KVB - 1);  // + the second kv_full / kv_empty
   static constexpr int SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr int COL_S = 0, COL_DP = 128, COL_DV = 256, COL_DK = 256 + D;
   static constexpr int COL_DQ = DQ_IN_DP ? COL_DP : 256 + 2 * D;
@@ -242,6 +262,9 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
   uint64_t* dq_free = s_full + 5;
   uint64_t* dkv_full = s_full + 6;
   uint64_t* kv_empty = s_full + 7;  // this item's K and V tiles are consumed
+  // K/V buffer b's barriers (the second pair after the others)
+  auto kvf = [&](int kb) { return kb == 0 ? kv_full : kv_empty + 1; };
+  auto kve = [&](int kb) { return kb == 0 ? kv_empty : kv_empty + 2; };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + T::NUM_BARS);
   float* lse_s = reinterpret_cast<float*>(smem + T::OFF_VEC);  // [2][128]
   float* del_s = lse_s + 256;                                   // [2][128]
@@ -307,6 +330,10 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
       ptx::mbar_init(dq_free, 4);  // one arrival per dQ-writer warp
       ptx::mbar_init(dkv_full, 1);
       ptx::mbar_init(kv_empty, 1);
+      if constexpr (T::KVB == 2) {
+        ptx::mbar_init(kvf(1), 1);
+        ptx::mbar_init(kve(1), 1);
+      }
       ptx::fence_mbar_init();
     }
     __syncwarp();
@@ -331,13 +358,15 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
         int itl = 0;
         for (int lin = item_of(0); lin < num_items; lin = item_of(++itl)) {
           const Item w = decode(lin);
-          if (itl > 0) ptx::mbar_wait(kv_empty, (itl - 1) & 1);
-          ptx::mbar_arrive_expect_tx(kv_full, 2 * T::TILE_BYTES);
+          const int kb = itl % T::KVB;
+          if (itl >= T::KVB) ptx::mbar_wait(kve(kb), ((itl / T::KVB) - 1) & 1);
+          BWD_IT(itl, 0);
+          ptx::mbar_arrive_expect_tx(kvf(kb), 2 * T::TILE_BYTES);
           for (int c = 0; c < D / 64; ++c) {
-            ptx::tma_load_4d(smem + T::OFF_K + c * T::CHUNK_BYTES, &tmK, kv_full, c * 64, w.hkv, w.j * 128,
-                             w.b, ptx::kEvictFirst);
-            ptx::tma_load_4d(smem + T::OFF_V + c * T::CHUNK_BYTES, &tmV, kv_full, c * 64, w.hkv, w.j * 128,
-                             w.b, ptx::kEvictFirst);
+            ptx::tma_load_4d(smem + T::OFF_K + kb * T::KV_STRIDE + c * T::CHUNK_BYTES, &tmK, kvf(kb), c * 64,
+                             w.hkv, w.j * 128, w.b, ptx::kEvictFirst);
+            ptx::tma_load_4d(smem + T::OFF_V + kb * T::KV_STRIDE + c * T::CHUNK_BYTES, &tmV, kvf(kb), c * 64,
+                             w.hkv, w.j * 128, w.b, ptx::kEvictFirst);
           }
 #if FA3B_BWD_KVPREFETCH
           // the next item's K / V into L2 now (its TMA load waits for kv_empty, this
@@ -384,8 +413,8 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
     } else if (warp == T::MMA_WARP) {
       // ------------------------------------------------ MMA issuer
       if (ptx::elect_one()) {
-        const uint32_t k_addr = ptx::smem_u32(smem + T::OFF_K);
-        const uint32_t v_addr = ptx::smem_u32(smem + T::OFF_V);
+        uint32_t k_addr = ptx::smem_u32(smem + T::OFF_K);
+        uint32_t v_addr = ptx::smem_u32(smem + T::OFF_V);
         const uint32_t ds_addr = ptx::smem_u32(smem + T::OFF_DS);
         auto tile_addr = [&](int t) { return ptx::smem_u32(smem + T::OFF_RING + slot_of(t) * T::TILE_BYTES); };
         auto wait_tile = [&](int t) {
@@ -415,12 +444,17 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
         int itl = 0;
         for (int lin = item_of(0); lin < num_items; lin = item_of(++itl)) {
           const Item w = decode(lin);
-          ptx::mbar_wait(kv_full, itl & 1);
+          const int kb = itl % T::KVB;
+          ptx::mbar_wait(kvf(kb), (itl / T::KVB) & 1);
+          BWD_IT(itl, 1);
+          k_addr = ptx::smem_u32(smem + T::OFF_K + kb * T::KV_STRIDE);
+          v_addr = ptx::smem_u32(smem + T::OFF_V + kb * T::KV_STRIDE);
           if (T::DQ_IN_DP && gi > 0) {  // the previous item's last dQ still sits in the dP^T columns
             ptx::mbar_wait(dq_free, (gi - 1) & 1);
           }
           wait_tile(2 * gi);
           issue_s(gi);
+          BWD_IT(itl, 2);
           ptx::mma_commit(s_full);
           wait_tile(2 * gi + 1);
           issue_dp(gi);
@@ -492,8 +526,9 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
               ptx::mma_commit(dp_full);
             }
           }
+          BWD_IT(itl, 3);
           ptx::mma_commit(dkv_full);
-          ptx::mma_commit(kv_empty);  // K and V of this item are no longer read
+          ptx::mma_commit(kve(kb));  // K and V of this item are no longer read
           gi += w.n_iter;
         }
       }
@@ -690,6 +725,7 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
     }
     // ------------------------------------------------ epilogue: dK, dV
     ptx::mbar_wait(dkv_full, itl & 1);
+    if (threadIdx.x == 0) BWD_IT(itl, 4);
     ptx::tc_fence_after();
     const bool row_ok = kv_row < N;
 #pragma unroll
@@ -722,6 +758,7 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
         }
       }
     }
+    if (threadIdx.x == 0) BWD_IT(itl, 5);
     }  // work items
   }
 
@@ -849,6 +886,10 @@ extern "C" {
 __attribute__((visibility("default"))) int fa3b_debug_bwd_trace(unsigned long long* out, int n) {
   const size_t bytes = sizeof(unsigned long long) * static_cast<size_t>(n);
   return cudaMemcpyFromSymbol(out, g_fa3b_bwd_trace, bytes) == cudaSuccess ? 0 : -1;
+}
+__attribute__((visibility("default"))) int fa3b_debug_bwd_items(unsigned long long* out, int n) {
+  const size_t bytes = sizeof(unsigned long long) * static_cast<size_t>(n);
+  return cudaMemcpyFromSymbol(out, g_fa3b_bwd_items, bytes) == cudaSuccess ? 0 : -1;
 }
 #endif
 
