@@ -170,6 +170,12 @@ struct BwdArgs {
 #ifndef FA3B_BWD_KV2
 #define FA3B_BWD_KV2 0
 #endif
+// FA3B_BWD_EPI_DQW: the dK / dV epilogue runs on the dQ-writer warpgroup, so the
+// gradient warps start the next work item at once (the MMA warp holds the next
+// item's first dV / dK MMA until the columns have been read out: dkv_free)
+#ifndef FA3B_BWD_EPI_DQW
+#define FA3B_BWD_EPI_DQW 1
+#endif
 template <int D_>
 struct BwdTraits {
   static constexpr int D = D_;
@@ -201,7 +207,8 @@ struct BwdTraits {
   static constexpr int OFF_BAR = OFF_VEC + 4 * 512;
   // kv_full, ring_full[RING], ring_empty[RING], vec_full[2], vec_empty[2], s_full,
   // dp_full, pa_full, pb_full, dq_full, dq_free, dkv_full, kv_empty
-  static constexpr int NUM_BARS = 13 + 2 * RING + 2 * (KVB - 1);  // + the second kv_full / kv_empty
+  // + the second kv_full / kv_empty, + dkv_free
+  static constexpr int NUM_BARS = 13 + 2 * RING + 2 * (KVB - 1) + 1;
   static constexpr int SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr int COL_S = 0, COL_DP = 128, COL_DV = 256, COL_DK = 256 + D;
   static constexpr int COL_DQ = DQ_IN_DP ? COL_DP : 256 + 2 * D;
@@ -265,6 +272,7 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
   // K/V buffer b's barriers (the second pair after the others)
   auto kvf = [&](int kb) { return kb == 0 ? kv_full : kv_empty + 1; };
   auto kve = [&](int kb) { return kb == 0 ? kv_empty : kv_empty + 2; };
+  uint64_t* dkv_free = kv_empty + 1 + 2 * (T::KVB - 1);  // dK / dV columns read out (EPI_DQW)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + T::NUM_BARS);
   float* lse_s = reinterpret_cast<float*>(smem + T::OFF_VEC);  // [2][128]
   float* del_s = lse_s + 256;                                   // [2][128]
@@ -334,6 +342,7 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
         ptx::mbar_init(kvf(1), 1);
         ptx::mbar_init(kve(1), 1);
       }
+      ptx::mbar_init(dkv_free, 4);  // one arrival per dQ-writer warp
       ptx::fence_mbar_init();
     }
     __syncwarp();
@@ -465,6 +474,8 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
             // dV += P^T dO (A = P^T pairs in TMEM, B = dO MN-major); then dO_i is free
             ptx::mbar_wait(pa_full, g & 1);
             if (itl == 0) BWD_TP(it, 0);
+            if (FA3B_BWD_EPI_DQW && it == 0 && itl > 0)  // the previous item's dK / dV read out
+              ptx::mbar_wait(dkv_free, (itl - 1) & 1);
             ptx::tc_fence_after();
             const uint32_t do_addr = tile_addr(2 * g + 1);
 #pragma unroll
@@ -611,6 +622,49 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
         }
       }
     }
+#if FA3B_BWD_EPI_DQW
+    // dK, dV of this item: TMEM -> bf16 rows (alpha folded into dK), then dkv_free
+    {
+      ptx::mbar_wait(dkv_full, itl & 1);
+      if (dw == 0 && lane == 0) BWD_IT(itl, 4);
+      ptx::tc_fence_after();
+      const int kv_row = w.j * 128 + r;
+      const bool row_ok = kv_row < N;
+#pragma unroll
+      for (int which = 0; which < 2; ++which) {
+        const float scale = which ? args.alpha : 1.f;
+        uint16_t* base = static_cast<uint16_t*>(which ? args.dk : args.dv);
+        const size_t off = which ? (b * args.dk_sb + static_cast<size_t>(kv_row) * args.dk_ss + w.hkv * args.dk_sh)
+                                 : (b * args.dv_sb + static_cast<size_t>(kv_row) * args.dv_ss + w.hkv * args.dv_sh);
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t ev[32];
+          ptx::tmem_ld32(tmem + lane_base + (which ? T::COL_DK : T::COL_DV) + c * 32, ev);
+          ptx::tmem_wait_ld();
+          if (!row_ok) continue;
+          uint32_t pk2[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const float a0 = __uint_as_float(ev[2 * e]) * scale, a1 = __uint_as_float(ev[2 * e + 1]) * scale;
+            pk2[e] = BF16 ? ptx::pack_bf16(a0, a1) : ptx::pack_f16(a0, a1);
+          }
+          uint16_t* orow = base + off + c * 32;
+          if (args.dkv_v8) {
+            ptx::st_global_v8(orow, &pk2[0]);
+            ptx::st_global_v8(orow + 16, &pk2[8]);
+          } else {
+            uint4* dst = reinterpret_cast<uint4*>(orow);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) dst[e] = make_uint4(pk2[4 * e], pk2[4 * e + 1], pk2[4 * e + 2], pk2[4 * e + 3]);
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(dkv_free);
+      if (dw == 0 && lane == 0) BWD_IT(itl, 5);
+    }
+#endif
     }  // work items
     if (leader) ptx::bulk_wait_group<0>();
   } else {
@@ -724,6 +778,7 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
       if (trc) BWD_TP(it, 7 + 4 * w);
     }
     // ------------------------------------------------ epilogue: dK, dV
+    if constexpr (!FA3B_BWD_EPI_DQW) {
     ptx::mbar_wait(dkv_full, itl & 1);
     if (threadIdx.x == 0) BWD_IT(itl, 4);
     ptx::tc_fence_after();
@@ -759,6 +814,7 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
       }
     }
     if (threadIdx.x == 0) BWD_IT(itl, 5);
+    }  // !FA3B_BWD_EPI_DQW
     }  // work items
   }
 
