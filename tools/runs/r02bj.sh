@@ -1,0 +1,8 @@
+set -u
+mkdir -p gpurun_out
+T=r02bj
+timeout 900 python -m pytest tests/test_fp8_gpu.py -x -q -k "prepare" > gpurun_out/${T}_pytest_prep.log 2>&1; echo "pytest prep rc=$?"
+for i in 1 2; do
+FA3B_LIB=build/variants/noism.so timeout 300 python tools/prep_time.py >> gpurun_out/${T}_prep.log 2>&1; echo "noism rc=$?"
+timeout 300 python tools/prep_time.py >> gpurun_out/${T}_prep.log 2>&1; echo "ism rc=$?"
+done
