@@ -218,6 +218,14 @@ struct BwdTraits {
 #ifndef FA3B_BWD_EMU128
 #define FA3B_BWD_EMU128 0
 #endif
+// FA3B_BWD_SPIN: the MMA warp's and the dQ writer's waits (pa/pb_full, dq_full,
+// dq_free) poll without the suspend hint: they sit on the iteration's critical
+// loop dK_i, dQ_i -> dQ drain -> dP_{i+1} -> phase B_{i+1}. Measured the same
+// as the suspend-hint waits (r02bm_spin_ab.log): ~140 cycles per hand-off either
+// way. Off.
+#ifndef FA3B_BWD_SPIN
+#define FA3B_BWD_SPIN 0
+#endif
 #ifndef FA3B_BWD_KVPREFETCH
 #define FA3B_BWD_KVPREFETCH 0
 #endif
@@ -228,6 +236,13 @@ struct BwdTraits {
   static constexpr int EMU = D == 64 ? FA3B_BWD_EMU64 : FA3B_BWD_EMU128;
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 };
+
+__device__ __forceinline__ void bwait(uint64_t* bar, uint32_t parity) {
+  if constexpr (FA3B_BWD_SPIN)
+    ptx::mbar_wait_nosleep(bar, parity);
+  else
+    ptx::mbar_wait(bar, parity);
+}
 
 // Deterministic dQ: wait until `want` KV tiles have added into this dQ tile, then
 // order the coming TMA reduce-adds after that observation; after issuing them,
@@ -459,7 +474,7 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
           k_addr = ptx::smem_u32(smem + T::OFF_K + kb * T::KV_STRIDE);
           v_addr = ptx::smem_u32(smem + T::OFF_V + kb * T::KV_STRIDE);
           if (T::DQ_IN_DP && gi > 0) {  // the previous item's last dQ still sits in the dP^T columns
-            ptx::mbar_wait(dq_free, (gi - 1) & 1);
+            bwait(dq_free, (gi - 1) & 1);
           }
           wait_tile(2 * gi);
           issue_s(gi);
@@ -472,7 +487,7 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
             const int g = gi + it;  // global iteration
             const bool more = it + 1 < w.n_iter;
             // dV += P^T dO (A = P^T pairs in TMEM, B = dO MN-major); then dO_i is free
-            ptx::mbar_wait(pa_full, g & 1);
+            bwait(pa_full, g & 1);
             if (itl == 0) BWD_TP(it, 0);
             if (FA3B_BWD_EPI_DQW && it == 0 && itl > 0)  // the previous item's dK / dV read out
               ptx::mbar_wait(dkv_free, (itl - 1) & 1);
@@ -494,7 +509,7 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
             }
 #endif
             // dK += dS^T Q (A = dS^T pairs in TMEM, B = Q MN-major); then Q_i, LSE2_i, D_i are free
-            ptx::mbar_wait(pb_full, g & 1);
+            bwait(pb_full, g & 1);
             if (itl == 0) BWD_TP(it, 1);
             ptx::tc_fence_after();
             const uint32_t q_addr = tile_addr(2 * g);
@@ -516,7 +531,7 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
             }
 #endif
             if (!T::DQ_IN_DP && g > 0) {  // own columns: the previous dQ must have been read out
-              ptx::mbar_wait(dq_free, (g - 1) & 1);
+              bwait(dq_free, (g - 1) & 1);
               ptx::tc_fence_after();
             }
 #pragma unroll
@@ -528,7 +543,7 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
             ptx::mma_commit(dq_full);
             if (more) {
               if (T::DQ_IN_DP) {  // dP_{i+1} overwrites the dQ_i columns once they are read out
-                ptx::mbar_wait(dq_free, g & 1);
+                bwait(dq_free, g & 1);
                 ptx::tc_fence_after();
               }
               if (itl == 0) BWD_TP(it, 2);
@@ -566,7 +581,7 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
       int* sem = args.dq_sem == nullptr
                      ? nullptr
                      : args.dq_sem + (static_cast<size_t>(b) * args.H + h) * (args.Npad / 128) + i;
-      ptx::mbar_wait(dq_full, gi & 1);
+      bwait(dq_full, gi & 1);
       if (itl == 0 && dw == 0 && lane == 0) BWD_TP(it, 12);
       ptx::tc_fence_after();
       uint32_t v[NB][32];

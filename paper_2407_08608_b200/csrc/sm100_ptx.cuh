@@ -104,6 +104,21 @@ __device__ __forceinline__ bool mbar_try_wait_sleep(uint32_t bar, uint32_t parit
       : "memory");
   return ok != 0;
 }
+// try_wait without the suspend hint (the hardware's own short wait per call),
+// with the same watchdog as mbar_wait: for latency-critical waiters.
+__device__ __forceinline__ void mbar_wait_nosleep(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  if (mbar_try_wait(a, parity)) return;
+#if FA3B_WATCHDOG
+  const long long t0 = clock64();
+  while (!mbar_try_wait(a, parity)) {
+    if (clock64() - t0 > (1ll << FA3B_WATCHDOG_LOG2)) __trap();
+  }
+#else
+  while (!mbar_try_wait(a, parity)) {
+  }
+#endif
+}
 // Spinning variant (no suspend) for a latency-critical single waiter.
 __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
