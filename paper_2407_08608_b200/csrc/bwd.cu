@@ -226,6 +226,14 @@ struct BwdTraits {
 #ifndef FA3B_BWD_SPIN
 #define FA3B_BWD_SPIN 0
 #endif
+// FA3B_BWD_DK_SS: dK_i = dS_i^T Q_i as an SS-MMA reading dS^T from the shared
+// dS tile (K-major view of the tile dQ reads MN-major) instead of a TS-MMA on
+// dS^T pairs in the dP^T columns, so dQ_i can be issued first and the dQ drain
+// and dP_{i+1} stop waiting behind dK_i. Measured 3-11 % slower (r02bn: the SS
+// operand traffic stretches phase A from ~1400 to ~1900 cycles per tile): off
+#ifndef FA3B_BWD_DK_SS
+#define FA3B_BWD_DK_SS 0
+#endif
 #ifndef FA3B_BWD_KVPREFETCH
 #define FA3B_BWD_KVPREFETCH 0
 #endif
@@ -508,21 +516,55 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
               ptx::mma_commit(s_full);
             }
 #endif
-            // dK += dS^T Q (A = dS^T pairs in TMEM, B = Q MN-major); then Q_i, LSE2_i, D_i are free
             bwait(pb_full, g & 1);
             if (itl == 0) BWD_TP(it, 1);
             ptx::tc_fence_after();
             const uint32_t q_addr = tile_addr(2 * g);
+            auto issue_dk = [&]() {
+#if FA3B_BWD_DK_SS
+              // dK += dS^T Q, A = dS^T K-major from the shared dS tile (the one dQ reads)
 #pragma unroll
-            for (int t = 0; t < 8; ++t)
-              ptx::mma_f16_ts(tmem + T::COL_DK, tmem + T::COL_DP + pair_col(t),
-                              ptx::sw128_desc(q_addr + t * 16 * 128, T::CHUNK_BYTES, 1024), idesc_acc,
-                              (it > 0 || t > 0));
-            ptx::mma_commit(&ring_empty[slot_of(2 * g)]);
-            if (T::VEC_OWN)
-              ptx::mma_commit(&vec_empty[g & 1]);
-            else
-              ptx::mma_commit(&ring_empty[slot_of(2 * g + 1)]);
+              for (int t = 0; t < 8; ++t)
+                ptx::mma_f16_ss(tmem + T::COL_DK,
+                                ptx::sw128_desc(ds_addr + (t >> 2) * T::CHUNK_BYTES + (t & 3) * 32, 16, 1024),
+                                ptx::sw128_desc(q_addr + t * 16 * 128, T::CHUNK_BYTES, 1024), idesc_acc,
+                                (it > 0 || t > 0));
+#else
+              // dK += dS^T Q (A = dS^T pairs in TMEM, B = Q MN-major)
+#pragma unroll
+              for (int t = 0; t < 8; ++t)
+                ptx::mma_f16_ts(tmem + T::COL_DK, tmem + T::COL_DP + pair_col(t),
+                                ptx::sw128_desc(q_addr + t * 16 * 128, T::CHUNK_BYTES, 1024), idesc_acc,
+                                (it > 0 || t > 0));
+#endif
+              // then Q_i, LSE2_i, D_i are free
+              ptx::mma_commit(&ring_empty[slot_of(2 * g)]);
+              if (T::VEC_OWN)
+                ptx::mma_commit(&vec_empty[g & 1]);
+              else
+                ptx::mma_commit(&ring_empty[slot_of(2 * g + 1)]);
+            };
+            auto issue_dq = [&]() {
+              if (!T::DQ_IN_DP && g > 0) {  // own columns: the previous dQ must have been read out
+                bwait(dq_free, (g - 1) & 1);
+                ptx::tc_fence_after();
+              }
+#pragma unroll
+              for (int t = 0; t < 8; ++t) {  // dQ = dS K: 16 KV rows per step, both operands MN-major
+                const uint32_t off = t * 16 * 128;
+                ptx::mma_f16_ss(tmem + T::COL_DQ, ptx::sw128_desc(ds_addr + off, T::CHUNK_BYTES, 1024),
+                                ptx::sw128_desc(k_addr + off, T::CHUNK_BYTES, 1024), idesc_dq, t > 0);
+              }
+              ptx::mma_commit(dq_full);
+            };
+#if FA3B_BWD_DK_SS
+            // dQ_i first: its drain (and, at d = 128, the dP_{i+1} that reuses its
+            // columns) then overlaps dK_i instead of following it
+            issue_dq();
+            issue_dk();
+#else
+            issue_dk();
+#endif
 #if !FA3B_BWD_S_EARLY
             if (more) {
               wait_tile(2 * g + 2);
@@ -530,17 +572,9 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
               ptx::mma_commit(s_full);
             }
 #endif
-            if (!T::DQ_IN_DP && g > 0) {  // own columns: the previous dQ must have been read out
-              bwait(dq_free, (g - 1) & 1);
-              ptx::tc_fence_after();
-            }
-#pragma unroll
-            for (int t = 0; t < 8; ++t) {  // dQ = dS K: 16 KV rows per step, both operands MN-major
-              const uint32_t off = t * 16 * 128;
-              ptx::mma_f16_ss(tmem + T::COL_DQ, ptx::sw128_desc(ds_addr + off, T::CHUNK_BYTES, 1024),
-                              ptx::sw128_desc(k_addr + off, T::CHUNK_BYTES, 1024), idesc_dq, t > 0);
-            }
-            ptx::mma_commit(dq_full);
+#if !FA3B_BWD_DK_SS
+            issue_dq();
+#endif
             if (more) {
               if (T::DQ_IN_DP) {  // dP_{i+1} overwrites the dQ_i columns once they are read out
                 bwait(dq_free, g & 1);
@@ -777,7 +811,8 @@ __global__ void __launch_bounds__(BwdTraits<D>::NUM_THREADS, 1)
           dk2[2 * c4] = BF16 ? ptx::pack_bf16(a.x, a.y) : ptx::pack_f16(a.x, a.y);
           dk2[2 * c4 + 1] = BF16 ? ptx::pack_bf16(bq.x, bq.y) : ptx::pack_f16(bq.x, bq.y);
         }
-        ptx::tmem_st16(tmem + lane_base + T::COL_DP + 64 * w + 16 * hf, dk2);
+        if constexpr (!FA3B_BWD_DK_SS)  // dK reads dS^T from TMEM (else from the shared tile)
+          ptx::tmem_st16(tmem + lane_base + T::COL_DP + 64 * w + 16 * hf, dk2);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int uu = 4 * hf + u;
