@@ -16,8 +16,9 @@
 //   warp 8*NT         TMA producer: Q tiles once, then K_j, V_j through a ring
 //                     of STAGES shared-memory slots
 //   warp 8*NT+1       MMA issuer (one elected thread), TMEM allocator
-// TMEM (512 columns): S_t at [128 t, 128 t + 128), P_t (16-bit, 2 per column)
-// aliased onto the first 64 columns of S_t, O_t at [128 NT + D t, + D).
+// TMEM (512 columns): S_t at [128 t, 128 t + 128), P_t (16-bit, 2 per column;
+// e4m3, 4 per column) aliased onto S_t, each softmax warpgroup's P over the first
+// columns of its own 64-column half (FwdTraits::p_kcol), O_t at [128 NT + D t, + D).
 //
 // Per tile the MMA order is  S(K_0) ; { PV(V_j) ; S(K_{j+1}) }_j , so the
 // arrival of S(K_{j+1}) implies PV(V_j) is complete (tcgen05.commit covers all
@@ -1191,8 +1192,8 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
       } else {
         exp_half((m_cur == -INFINITY) ? 0.f : m_cur);
       }
-      // P (packed, key order) over the first columns of this block's S buffer; every
-      // split's S load has completed (the exchange barrier above)
+      // P (packed, key order) over the first columns of this warpgroup's own S
+      // columns (FwdTraits::p_kcol), which only this thread's row has read
       if constexpr (FA3B_FWD_PSPLIT && NPK >= 16) {
         if constexpr (NPK == 16)
           ptx::tmem_st8(tS + HC * hh + 8, *reinterpret_cast<uint32_t(*)[8]>(&pk[8]));
