@@ -130,6 +130,29 @@ def test_fp8_gqa_and_batch(port, cuda):
             assert torch.equal(oo[0, :, 0], o[b, :, h]) and torch.equal(ll[0, 0], lse[b, h])
 
 
+@pytest.mark.parametrize("D,causal", [(128, False), (64, True), (256, True)])
+def test_fp8_negative_alpha_equals_negated_keys(cuda, D, causal):
+    """alpha < 0 (the reference accepts any finite nonzero alpha,
+    attention_ref.cpp:27-28) flips the QK^T sign in the MMA instruction: with
+    e4m3 codes symmetric and RNE accumulation, fp8_fwd(alpha = -a) equals
+    fp8_fwd(-K, alpha = +a) bit for bit (Hadamard, block scales and all)."""
+    from paper_2407_08608_b200 import api
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(D + causal)
+    q, k, v = (torch.randn(2, 300, 2, D, device="cuda", generator=g, dtype=torch.bfloat16) for _ in range(3))
+    a = 0.7 / math.sqrt(D)
+    o1, l1 = api.fp8_fwd(q, k, v, causal=causal, alpha=-a, seed=5)
+    o2, l2 = api.fp8_fwd(q, -k, v, causal=causal, alpha=a, seed=5)
+    assert torch.equal(o1, o2) and torch.equal(l1, l2)
+    # and against fp32 attention with the negative scale
+    s = -a * q[0, :, 1].float() @ k[0, :, 1].float().T
+    if causal:
+        s = s.masked_fill(torch.arange(300, device="cuda")[None, :] > torch.arange(300, device="cuda")[:, None],
+                          -math.inf)
+    ref = torch.softmax(s, -1) @ v[0, :, 1].float()
+    assert (o1[0, :, 1].float() - ref).norm().item() < 0.05 * ref.norm().item()
+
+
 def test_fp8_rejects_bad_blocks(cuda):
     from paper_2407_08608_b200 import api
     from paper_2407_08608_b200._lib import Fa3bError
