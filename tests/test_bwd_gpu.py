@@ -68,6 +68,10 @@ CASES = [
     # long GQA groups: the Q/dO ring and the LSE/D buffers wrap many times within a CTA
     pytest.param(1, 8, 1, 640, 128, True, "bf16", None, id="gqa8-ring-d128"),
     pytest.param(1, 4, 1, 520, 64, False, "fp16", None, id="gqa4-ring-d64"),
+    # tiny and ragged lengths: one valid row / one row past a tile boundary
+    pytest.param(2, 2, 2, 1, 128, True, "bf16", None, id="n1-d128"),
+    pytest.param(1, 2, 1, 1, 64, False, "bf16", None, id="n1-d64-gqa"),
+    pytest.param(1, 2, 2, 129, 128, True, "bf16", None, id="n129-causal"),
 ]
 
 
@@ -82,10 +86,19 @@ def test_bwd_matches_oracle(port, cuda, B, H, Hkv, N, D, causal, fmt, alpha):
     dq, dk, dv = api.bwd(to_dev(q, dt), to_dev(k, dt), to_dev(v, dt), to_dev(o, dt),
                          to_dev(do, dt), torch.from_numpy(lse).float().cuda(), causal=causal,
                          alpha=alpha)
+    scale = float(np.sqrt(np.mean(ex[2] ** 2)))  # dV's RMS: the gradients' natural size
     for name, got, e, m in zip(("dq", "dk", "dv"), (dq, dk, dv), ex, em):
         got = got.float().cpu().numpy()
+        if float(np.sqrt(np.mean(e ** 2))) < 1e-6 * scale:
+            # N = 1: dS = P (dP - D) is exactly 0 (one key, P = 1, O = V), so dQ and dK
+            # are rounding noise of the 16-bit O: absolute, against the emulation's
+            assert rmse(got, e) <= 2 * rmse(m, e) + 1e-3 * scale, (name, rmse(got, e), rmse(m, e))
+            continue
         r_gpu, r_emu = _rel(got, e), _rel(m, e)
-        assert r_gpu <= 2 * r_emu + 1e-5, (name, r_gpu, r_emu)
+        # + the rounding of the 16-bit gradient outputs (the emulation keeps FP64
+        # outputs: at N = 1 with GQA its dV is exact, the device's is one RN away)
+        out_rn = 2.0 ** -8 if fmt == "bf16" else 2.0 ** -11
+        assert r_gpu <= 2 * r_emu + out_rn, (name, r_gpu, r_emu)
 
 
 def test_bwd_end_to_end_with_device_forward(port, cuda):
