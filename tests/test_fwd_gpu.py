@@ -314,7 +314,7 @@ def test_one_tile_double_buffered_s(cuda, B, N, H, Hkv, D, causal, sched):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("D", [64, 256])
+@pytest.mark.parametrize("D", [64, 128, 256])
 @pytest.mark.parametrize("causal", [False, True])
 def test_tiny_and_ragged_lengths_buffer_rotation(cuda, D, causal):
     """The S-buffer schedules (three rotating buffers at d64, two at d256) at every
