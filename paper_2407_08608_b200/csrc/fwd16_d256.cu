@@ -11,3 +11,11 @@ int launch_fwd16_default_d256(const fa3b_fwd_params& p, cudaStream_t s, bool cta
 }
 
 }  // namespace fa3b
+
+#ifdef FA3B_TRACE
+// Debug builds only (-DFA3B_TRACE): the phase points recorded by the d = 256 forward.
+extern "C" __attribute__((visibility("default"))) int fa3b_debug_trace_d256(unsigned long long* out, int n) {
+  const size_t bytes = sizeof(unsigned long long) * static_cast<size_t>(n);
+  return cudaMemcpyFromSymbol(out, fa3b::g_fa3b_trace, bytes) == cudaSuccess ? 0 : -1;
+}
+#endif

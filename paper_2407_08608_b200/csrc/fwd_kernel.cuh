@@ -97,6 +97,19 @@
 #ifndef FA3B_FWD_SPEC
 #define FA3B_FWD_SPEC 0
 #endif
+// FA3B_FWD_CHRING: with 64 KB K/V tiles (bf16 d = 256, one-tile S2 schedule, a
+// 2-tile ring) the ring is managed per 16 KB column chunk: each chunk has its own
+// full/empty barrier, the S MMA consumes K chunk by chunk and PV runs as one
+// N = 64 MMA group per V chunk, so loads refill freed chunks while the rest of
+// the tile is still in use and an MMA starts as soon as its first chunk lands
+#ifndef FA3B_FWD_CHRING
+#define FA3B_FWD_CHRING 1
+#endif
+// also the FP8 d = 256 tiles (32 KB, 4-tile ring): measured 6 % slower there
+// (r02cb_chring8_ab.log), off; bf16 d = 256: +11-14 % (r02ca_chring_ab.log)
+#ifndef FA3B_FWD_CHRING_FP8
+#define FA3B_FWD_CHRING_FP8 0
+#endif
 // release Q after the item's last S (not after its last PV): see the MMA warp
 #ifndef FA3B_FWD_QEARLY
 #define FA3B_FWD_QEARLY 1
@@ -282,11 +295,14 @@ struct FwdTraits {
   static_assert(!NOWS || STAGES >= 4, "no-WS schedule needs a 4-stage K/V ring");
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_KV = QB * NT * TILE_BYTES;
+  // chunk-granular ring (FA3B_FWD_CHRING): RSLOTS barrier pairs of KV_CHUNK_BYTES
+  static constexpr bool CH = S2 && FA3B_FWD_CHRING && D == 256 && FA3B_FWD_CHRING_FP8 >= (EB == 1 ? 1 : 0);
+  static constexpr int RSLOTS = CH ? STAGES * CHUNKS : STAGES;
   static constexpr int OFF_BAR = OFF_KV + STAGES * KV_TILE_BYTES;
   // q_full, kv_full[S], kv_empty[S], s_full[2 NT], p_full[NT], o_full[NT], q_empty,
   // pv_done[NT] (the second s_full per tile and pv_done serve S2 / S3), then (QB = 2)
   // the second buffer's q_full, q_empty
-  static constexpr int NUM_BARS = 3 + 2 * STAGES + 5 * NT + (QB == 2 ? 2 : 0);
+  static constexpr int NUM_BARS = 3 + 2 * RSLOTS + 5 * NT + (QB == 2 ? 2 : 0);
   // row-max / row-sum exchange between the column splits: [NT][2 buf][NQ][128]
   static constexpr int OFF_XCH = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr int SMEM_BYTES = OFF_XCH + NT * 2 * NQ * 128 * 4 + 1024;
@@ -458,8 +474,8 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + T::OFF_BAR);
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;
-  uint64_t* kv_empty = kv_full + T::STAGES;
-  uint64_t* s_full = kv_empty + T::STAGES;
+  uint64_t* kv_empty = kv_full + T::RSLOTS;
+  uint64_t* s_full = kv_empty + T::RSLOTS;
   uint64_t* p_full = s_full + 2 * NT;  // S2 / S3: s_full[2 t + (S count of tile t & 1)]
   uint64_t* o_full = p_full + NT;
   uint64_t* q_empty = o_full + NT;  // the Q tiles of a work item are consumed
@@ -524,7 +540,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
   if (warp == T::ALLOC_WARP) {
     if (ptx::lane_id() == 0) {
       ptx::mbar_init(q_full, 1);
-      for (int s = 0; s < T::STAGES; ++s) {
+      for (int s = 0; s < T::RSLOTS; ++s) {
         ptx::mbar_init(&kv_full[s], 1);
         ptx::mbar_init(&kv_empty[s], 1);
       }
@@ -603,6 +619,18 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
           }
         };
         auto load_kv = [&](bool is_v, int blk) {
+          if constexpr (T::CH) {
+#pragma unroll
+            for (int c = 0; c < T::CHUNKS; ++c) {
+              const int ci = item * T::CHUNKS + c, cs = ci % T::RSLOTS;
+              ptx::mbar_wait(&kv_empty[cs], ((ci / T::RSLOTS) & 1) ^ 1);
+              ptx::mbar_arrive_expect_tx(&kv_full[cs], T::KV_CHUNK_BYTES);
+              ptx::tma_load_4d(smem + T::OFF_KV + cs * T::KV_CHUNK_BYTES, is_v ? &tmV : &tmK, &kv_full[cs],
+                               c * T::CHUNK_ELEMS, w.hkv, blk * T::BN, w.b, ptx::kEvictLast);
+            }
+            ++item;
+            return;
+          }
           const int slot = item % T::STAGES;
           const uint32_t ph = (item / T::STAGES) & 1;
           ptx::mbar_wait(&kv_empty[slot], ph ^ 1);
@@ -731,6 +759,70 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
             ptx::tc_fence_after();
             return pos++ % T::STAGES;
           };
+          if constexpr (T::CH) {
+            // chunk-granular ring: tile position p's chunk c sits in chunk slot
+            // (p CHUNKS + c) % RSLOTS with its own barriers
+            auto chunk_wait = [&](int p, int c) {
+              const int ci = p * T::CHUNKS + c, cs = ci % T::RSLOTS;
+              ptx::mbar_wait(&kv_full[cs], (ci / T::RSLOTS) & 1);
+              ptx::tc_fence_after();
+              return cs;
+            };
+            auto s_issue_ch = [&](int p) {
+              const uint32_t scol = T::s2_col(gs & 1);
+#pragma unroll
+              for (int c = 0; c < T::CHUNKS; ++c) {
+                const int cs = chunk_wait(p, c);
+#pragma unroll
+                for (int kk = 0; kk < T::KPR; ++kk) {
+                  const int k = c * T::KPR + kk;
+                  const uint64_t a = ptx::swz_desc<T::ROW_BYTES>(q_cur + c * T::CHUNK_BYTES + kk * 32, 16, T::SBO);
+                  const uint64_t bd =
+                      ptx::swz_desc<T::ROW_BYTES>(kv_addr + cs * T::KV_CHUNK_BYTES + kk * 32, 16, T::SBO);
+                  if constexpr (FP8)
+                    ptx::mma_f8_ss(tmem + scol, a, bd, idesc_qk, k > 0 ? 1u : 0u);
+                  else
+                    ptx::mma_f16_ss(tmem + scol, a, bd, idesc_qk, k > 0 ? 1u : 0u);
+                }
+                ptx::mma_commit(&kv_empty[cs]);
+              }
+              ptx::mma_commit(&s_full[gs & 1]);
+              ++gs;
+            };
+            // PV per V chunk: N = CHUNK_ELEMS columns of O
+            const uint32_t idesc_pv_c = (idesc_pv & ~(0x3Fu << 17)) | ((T::CHUNK_ELEMS >> 3) << 17);
+            auto pv_issue_ch = [&](int p, bool acc, uint32_t scol) {
+              ptx::mbar_wait(&p_full[0], pc[0]++ & 1);
+              ptx::tc_fence_after();
+#pragma unroll
+              for (int c = 0; c < T::CHUNKS; ++c) {
+                const int cs = chunk_wait(p, c);
+#pragma unroll
+                for (int k = 0; k < T::BN / KSTEP; ++k) {
+                  const uint64_t bd = ptx::swz_desc<T::ROW_BYTES>(
+                      kv_addr + cs * T::KV_CHUNK_BYTES + k * KSTEP * T::ROW_BYTES, T::KV_CHUNK_BYTES, T::SBO);
+                  if constexpr (FP8)
+                    ptx::mma_f8_ts(tmem + T::o_col(0) + c * T::CHUNK_ELEMS, tmem + scol + T::p_kcol(k, KSTEP), bd,
+                                   idesc_pv_c, (acc || k > 0) ? 1u : 0u);
+                  else
+                    ptx::mma_f16_ts(tmem + T::o_col(0) + c * T::CHUNK_ELEMS, tmem + scol + T::p_kcol(k, KSTEP), bd,
+                                    idesc_pv_c, (acc || k > 0) ? 1u : 0u);
+                }
+                ptx::mma_commit(&kv_empty[cs]);
+              }
+            };
+            for (int j = 0; j < 2 && j < n; ++j) s_issue_ch(pos++);
+            for (int j = 0; j < n; ++j) {
+              pv_issue_ch(pos++, j > 0, T::s2_col((g0 + j) & 1));
+              if (itl == 0) FA3B_TP(0, j, 6);
+              ptx::mma_commit(&pv_done[0]);
+              if (j + 1 == n) ptx::mma_commit(&o_full[0]);
+              if (j + 2 < n) s_issue_ch(pos++);
+            }
+            ptx::mma_commit(qe(itl));
+            kvi += 2 * n;
+            continue;
+          }
           for (int j = 0; j < 2 && j < n; ++j) {
             const int slot = wait_pos();
             s_issue(slot);

@@ -19,7 +19,7 @@ for _ in range(3): run()
 torch.cuda.synchronize()
 lib = _lib.load()
 buf = (ctypes.c_ulonglong * (2 * 64 * 8))()
-acc = lib.fa3b_debug_trace_fp8 if fp8 else (lib.fa3b_debug_trace_d64 if D == 64 else lib.fa3b_debug_trace)
+acc = lib.fa3b_debug_trace_fp8 if fp8 else {64: lib.fa3b_debug_trace_d64, 256: lib.fa3b_debug_trace_d256}.get(D, lib.fa3b_debug_trace)
 assert acc(buf, 2 * 64 * 8) == 0
 t = np.frombuffer(buf, dtype=np.uint64).reshape(2, 64, 8).astype(np.int64)
 base = t[t > 0].min()
