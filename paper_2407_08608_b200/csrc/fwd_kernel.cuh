@@ -1312,6 +1312,7 @@ __global__ void __launch_bounds__(FwdTraits<D, NT, KIND == KIND_E4M3 ? 1 : 2, CP
         if (j > 0) ptx::mbar_wait(&pv_done[t], (sc - 2) & 1);
       // PV(V_{j-1}) is complete (see header / above); rescale this thread's O_t columns.
       if (j > 0 && __any_sync(0xffffffffu, ofac != 1.f)) rescale_o(ofac);
+      if (tr) FA3B_TP(t, j, 7);
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
       __syncwarp();
