@@ -107,6 +107,9 @@
 #endif
 // also the FP8 d = 256 tiles (32 KB, 4-tile ring): measured 6 % slower there
 // (r02cb_chring8_ab.log), off; bf16 d = 256: +11-14 % (r02ca_chring_ab.log)
+#ifndef FA3B_FWD_CHRING_EXTRA
+#define FA3B_FWD_CHRING_EXTRA 0
+#endif
 #ifndef FA3B_FWD_CHRING_FP8
 #define FA3B_FWD_CHRING_FP8 0
 #endif
@@ -297,8 +300,11 @@ struct FwdTraits {
   static constexpr int OFF_KV = QB * NT * TILE_BYTES;
   // chunk-granular ring (FA3B_FWD_CHRING): RSLOTS barrier pairs of KV_CHUNK_BYTES
   static constexpr bool CH = S2 && FA3B_FWD_CHRING && D == 256 && FA3B_FWD_CHRING_FP8 >= (EB == 1 ? 1 : 0);
-  static constexpr int RSLOTS = CH ? STAGES * CHUNKS : STAGES;
-  static constexpr int OFF_BAR = OFF_KV + STAGES * KV_TILE_BYTES;
+  // (+ FA3B_FWD_CHRING_EXTRA chunk slots where shared memory allows: chunks
+  // are independent, so the ring need not hold a whole number of tiles; one extra
+  // measured no gain, r02ch_chx_ab.log)
+  static constexpr int RSLOTS = CH ? STAGES * CHUNKS + FA3B_FWD_CHRING_EXTRA : STAGES;
+  static constexpr int OFF_BAR = OFF_KV + (CH ? RSLOTS * KV_CHUNK_BYTES : STAGES * KV_TILE_BYTES);
   // q_full, kv_full[S], kv_empty[S], s_full[2 NT], p_full[NT], o_full[NT], q_empty,
   // pv_done[NT] (the second s_full per tile and pv_done serve S2 / S3), then (QB = 2)
   // the second buffer's q_full, q_empty
