@@ -27,7 +27,8 @@ def bench(fn, iters=30):
 
 
 tag = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith("FA3B_"))
-pts = [(d, n, c, dt) for dt in ("bf16", "e4m3") for d in (128, 64) for n in (2048, 8192)
+DIMS = [int(x) for x in os.environ.get("AB_DIMS", "128,64").split(",")]
+pts = [(d, n, c, dt) for dt in ("bf16", "e4m3") for d in DIMS for n in (2048, 8192)
        for c in (False, True) if not (dt == "e4m3" and d == 64)]
 for d, n, causal, dt in pts:
     B, H = 16384 // n, 2048 // d
